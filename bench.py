@@ -1,0 +1,489 @@
+#!/usr/bin/env python
+"""Benchmark of the Double Sparsity decode hot path on B200 (BASELINE.json metric:
+"sparse decode-attn us/layer & HBM GB/s vs dense, S=32K, 1/16 sparsity, 1-8 B200").
+
+A step = one decode step of the whole hot path over L resident layer caches:
+per layer a0 (ds_append_kv of the current token) + a1..a5 (ds_decode_attention).
+Workload at N=1: c3 (Llama-3-8B GQA, B=16, H_q=32, H_kv=8, d=128, S=32768,
+r=8, k=2048, bf16) -- the config BASELINE.json's metric names (S=32K, 1-8 B200).
+N>1 (torchrun, one rank per GPU): weak scaling, every rank runs its own c3
+batch (independent units, no data-path collective); --mode allgather instead
+shards c3's KV heads over the ranks and all-gathers the head outputs over NCCL
+(strong scaling, north_star's variant).
+
+value = algorithmic HBM bytes (label S*r*e + gathered K/V 2*k*d*e per unit,
+SURVEY 8(d)) of all layers of all ranks / max-over-ranks device time, GB/s.
+Inputs are resident in HBM; every step touches L x 192 MiB >> 126 MB L2.
+
+--impl reference: the CPU oracle (oracle/) timed on the host cores on bounded
+samples of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2408_07092_b200 import ledger  # noqa: E402
+
+METRIC = "sparse decode-attn µs/layer & HBM GB/s vs dense, S=32K, 1/16 sparsity, 1-8 B200"
+KERNELS_PER_APPEND = 1
+KERNELS_PER_DECODE = 3      # score+select (cluster), split-K attention, combine
+KERNELS_PER_DENSE = 2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--layers", type=int, default=8)
+    ap.add_argument("--structure", default="iid", choices=["iid", "clustered"])
+    ap.add_argument("--mode", default="weak", choices=["weak", "allgather"])
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--extra", action="store_true", help="also time c2 S=4K/16K/32K (reported under 'extra')")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------- dist plumbing
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, backend):
+        if self.world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group(backend=backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            if torch.cuda.is_available():
+                self.pg.barrier(device_ids=[self.local])
+            else:
+                self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def done(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+def shard_plan(cfg: synth.Config, world: int, rank: int, mode: str):
+    """Units a rank owns.  weak: a full cfg batch per rank (seeded by rank).
+    allgather: a contiguous slice of KV heads (and their G query heads)."""
+    if mode == "weak" or world == 1:
+        return cfg, 0
+    if cfg.Hkv % world != 0:
+        raise SystemExit(f"--mode allgather needs H_kv ({cfg.Hkv}) divisible by {world}")
+    hk = cfg.Hkv // world
+    return cfg.with_(Hkv=hk, Hq=cfg.G * hk), rank * hk
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    def __init__(self, gpu_index: int, path: str):
+        self.path = path
+        self.proc = None
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        rows = []
+        for ln in open(self.path):
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) >= 9 and p[1].replace(".", "").isdigit():
+                rows.append(p)
+        if not rows:
+            return None
+        sm = [float(p[1]) for p in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for p in rows for i in range(4) if "Active" in p[5 + i]})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(p[3]) for p in rows if p[3].replace(".", "").isdigit())
+                if any(p[3].replace(".", "").isdigit() for p in rows) else None}
+
+
+# ----------------------------------------------------------- our GPU arm
+def build_layers(cfg, L, rank, structure, device):
+    import paper_2408_07092_b200 as ds
+    layers = []
+    for l in range(L):
+        seed = cfg.seed_base + 97 * rank + l
+        lay = synth.make_layer(cfg, seed, device=device, structure=structure)
+        Qc, Kc = synth.make_calibration(cfg, n=512, seed=seed, device=device)
+        C = ds.ds_calibrate_channels(Qc, Kc, cfg.Hkv, cfg.r)            # offline, untimed
+        cache = ds.LayerCache.allocate(cfg.B, cfg.Hq, cfg.Hkv, cfg.d, cfg.S, cfg.r, synth.DTYPES[cfg.dtype],
+                                       lay.block_table, num_pages=lay.num_pages, page_size=cfg.page_size,
+                                       device=device, channel_idx=C)
+        ds.prefill(cache, lay.K, lay.V, lay.seq_lens)
+        # the decode step's inputs: the current token (position S-1) and its query
+        k_new = lay.K[:, :, cfg.S - 1:cfg.S].transpose(1, 2).contiguous()
+        v_new = lay.V[:, :, cfg.S - 1:cfg.S].transpose(1, 2).contiguous()
+        pos = torch.full((cfg.B,), cfg.S - 1, dtype=torch.int32, device=device)
+        layers.append(dict(cache=cache, cs=cache.struct(), q=lay.q.contiguous(), k_new=k_new, v_new=v_new,
+                           pos=pos, out=torch.empty_like(lay.q)))
+        del lay, Qc, Kc
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return layers
+
+
+def time_graph(fn, steps, warmup, dist, stream):
+    """Capture fn() in a CUDA graph, replay W times, then time exactly K replays
+    with events on the capture stream (barrier + sync on both sides)."""
+    with torch.cuda.stream(stream):
+        fn()                                   # eager warm-up (attribute setup, allocator)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        fn()
+    for _ in range(warmup):
+        g.replay()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    return e0.elapsed_time(e1), g
+
+
+def run_ours(args, dist):
+    import paper_2408_07092_b200 as ds
+    dev = torch.device("cuda", dist.local)
+    torch.cuda.set_device(dev)
+    full = synth.CONFIGS[args.config]
+    cfg, h0 = shard_plan(full, dist.world, dist.rank, args.mode)
+    L = args.layers
+    hbm_peak, peak_src = peaks()
+    layers = build_layers(cfg, L, dist.rank if args.mode == "weak" else 0, args.structure, dev)
+    k = cfg.k
+    ws = ds.workspace(ds.ds_decode_workspace_size(layers[0]["cache"], k), dev)
+    stream = torch.cuda.Stream(dev)
+    gathered = None
+    if args.mode == "allgather" and dist.world > 1:
+        gathered = [torch.empty((dist.world,) + tuple(layers[0]["out"].shape), dtype=layers[0]["out"].dtype,
+                                device=dev) for _ in range(L)]
+    lib = ds.lib()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    P = ctypes.c_void_p
+
+    def step():
+        for i, ly in enumerate(layers):
+            ds._check(lib.ds_append_kv(ctypes.byref(ly["cs"]), P(ly["k_new"].data_ptr()), P(ly["v_new"].data_ptr()),
+                                       P(ly["pos"].data_ptr()), 1, sp), "append")
+            ds._check(lib.ds_decode_attention(ctypes.byref(ly["cs"]), P(ly["q"].data_ptr()), k,
+                                              P(ly["out"].data_ptr()), None, P(ws.data_ptr()), ws.numel(), sp),
+                      "decode")
+            if gathered is not None:
+                dist.pg.all_gather_into_tensor(gathered[i], ly["out"])
+
+    def decode_only():
+        for ly in layers:
+            lib.ds_decode_attention(ctypes.byref(ly["cs"]), P(ly["q"].data_ptr()), k, P(ly["out"].data_ptr()), None,
+                                    P(ws.data_ptr()), ws.numel(), sp)
+
+    clk = Clocks(dist.local, os.path.join(ROOT, "gpurun_out", f"clocks_rank{dist.rank}.csv")) \
+        if dist.rank == 0 else None
+    ms_total, _ = time_graph(step, args.steps, args.warmup, dist, stream)
+    clocks = clk.stop() if clk else None
+    ms_step = dist.max(ms_total / args.steps)
+
+    # dominant launch group for the roofline: ds_decode_attention alone over the same layers
+    ms_dec_total, _ = time_graph(decode_only, args.steps, 2, dist, stream)
+    us_decode = ms_dec_total / args.steps / L * 1000.0
+
+    bytes_layer = ledger.layer_bytes_alg(cfg)
+    n_ranks = dist.world
+    total_bytes = bytes_layer * L * (n_ranks if args.mode == "weak" else 1) if args.mode == "weak" else \
+        ledger.layer_bytes_alg(full) * L
+    value = total_bytes / (ms_step / 1e3) / 1e9
+    us_layer = ms_step * 1000.0 / L
+    res = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": n_ranks, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
+        "scaling": "weak" if args.mode == "weak" else "strong", "vs_baseline": None, "dtype": cfg.dtype,
+        "data": "synthetic (seeded N(0,1) q/K/V, 8 planted outlier channels per KV head, random page order)",
+        "config": {"workload": f"{full.name}: B={full.B} Hq={full.Hq} Hkv={full.Hkv} d={full.d} S={full.S} "
+                               f"r={full.r} k={full.k} {full.dtype}", "layers_resident": L,
+                   "structure": args.structure, "page_size": cfg.page_size,
+                   "parallelism": (f"dp{n_ranks}" if args.mode == "weak" else f"kv-head-shard{n_ranks}+allgather"),
+                   "l2": f"inputs > L2: each step touches {L} x {bytes_layer / 2**20:.0f} MiB of distinct layer caches"},
+        "us_per_layer": round(us_layer, 3),
+        "tokens_per_s_attn": round(full.B * (n_ranks if args.mode == "weak" else 1) * 1e6 / (us_layer * 32), 1),
+        "bytes_alg_per_layer": bytes_layer,
+    }
+    achieved = bytes_layer / (us_decode * 1e-6) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{full.name}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch_group")
+        except Exception:
+            traffic = None
+    res["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                       "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                       "kernel": "ds_decode_attention launch group (score_select + attn_split + combine)",
+                       "us_per_launch": round(us_decode, 3), "peak_source": peak_src,
+                       "algorithmic_bytes_per_launch": bytes_layer}
+    res["gpu_launches"] = args.steps * L * (KERNELS_PER_APPEND + KERNELS_PER_DECODE)
+    if clocks:
+        res["clocks"] = clocks
+
+    if not args.no_dense:
+        dws = ds.workspace(ds.ds_dense_workspace_size(layers[0]["cache"]), dev)
+
+        def dense():
+            for ly in layers:
+                lib.ds_dense_decode_attention(ctypes.byref(ly["cs"]), P(ly["q"].data_ptr()), P(ly["out"].data_ptr()),
+                                              P(dws.data_ptr()), dws.numel(), sp)
+        dsteps = max(3, args.steps // 4)
+        ms_d, _ = time_graph(dense, dsteps, 2, dist, stream)
+        us_dense = dist.max(ms_d / dsteps) * 1000.0 / L
+        res["dense_us_per_layer"] = round(us_dense, 3)
+        res["dense_gbs"] = round(ledger.layer_bytes_dense(cfg) / (us_dense * 1e-6) / 1e9, 1)
+        res["speedup_vs_dense"] = round(us_dense / us_decode, 3)
+        res["byte_ratio_ceiling"] = round(ledger.byte_ratio_ceiling(cfg), 3)
+        del dws
+
+    if not args.no_e2e:
+        res["e2e"] = e2e(args, dist, layers, ws, k, stream, cfg)
+    if args.extra and dist.world == 1:
+        res["extra"] = extra_configs(args)
+    del layers
+    torch.cuda.empty_cache()
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(full, budget_s=12.0)
+    return res
+
+
+def e2e(args, dist, layers, ws, k, stream, cfg):
+    """Same metric through the public Python API with host buffers: per step the
+    current token's q/k_new/v_new of every layer are copied from pinned host
+    memory and every layer's output is read back, inside the timed region."""
+    import paper_2408_07092_b200 as ds
+    hq = [ly["q"].cpu().pin_memory() for ly in layers]
+    hk = [ly["k_new"].cpu().pin_memory() for ly in layers]
+    hv = [ly["v_new"].cpu().pin_memory() for ly in layers]
+    ho = [torch.empty(ly["out"].shape, dtype=ly["out"].dtype).pin_memory() for ly in layers]
+    h2d = sum(t.numel() * t.element_size() for t in hq + hk + hv)
+    d2h = sum(t.numel() * t.element_size() for t in ho)
+
+    def one():
+        for i, ly in enumerate(layers):
+            ly["q"].copy_(hq[i], non_blocking=True)
+            ly["k_new"].copy_(hk[i], non_blocking=True)
+            ly["v_new"].copy_(hv[i], non_blocking=True)
+            ds.ds_append_kv(ly["cache"], ly["k_new"], ly["v_new"], ly["pos"], cs=ly["cs"])
+            ds.ds_decode_attention(ly["cache"], ly["q"], k, out=ly["out"], ws=ws, cs=ly["cs"])
+            ho[i].copy_(ly["out"], non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, args.warmup)):
+            one()
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            one()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = dist.max(e0.elapsed_time(e1) / args.steps)
+    L = len(layers)
+    nr = dist.world if args.mode == "weak" else 1
+    val = ledger.layer_bytes_alg(cfg) * L * nr / (ms / 1e3) / 1e9 if args.mode == "weak" else \
+        ledger.layer_bytes_alg(synth.CONFIGS[args.config]) * L / (ms / 1e3) / 1e9
+    return {"value": round(val, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": round(ms, 5), "api": "paper_2408_07092_b200.ds_append_kv + ds_decode_attention (eager)"}
+
+
+def extra_configs(args):
+    """c2 (Llama-2-7B MHA, B=1, fp16) at S=4K/16K/32K: us/layer sparse vs dense."""
+    import paper_2408_07092_b200 as ds
+    out = {}
+    stream = torch.cuda.Stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    P = ctypes.c_void_p
+    lib = ds.lib()
+
+    class _D:
+        def barrier(self):
+            pass
+    for name in ("c2_4k", "c2_16k", "c2_32k"):
+        cfg = synth.CONFIGS[name]
+        L = 32
+        layers = build_layers(cfg, L, 0, "iid", torch.device("cuda"))
+        ws = ds.workspace(ds.ds_decode_workspace_size(layers[0]["cache"], cfg.k))
+        dws = ds.workspace(ds.ds_dense_workspace_size(layers[0]["cache"]))
+
+        def dec():
+            for ly in layers:
+                lib.ds_decode_attention(ctypes.byref(ly["cs"]), P(ly["q"].data_ptr()), cfg.k, P(ly["out"].data_ptr()),
+                                        None, P(ws.data_ptr()), ws.numel(), sp)
+
+        def den():
+            for ly in layers:
+                lib.ds_dense_decode_attention(ctypes.byref(ly["cs"]), P(ly["q"].data_ptr()), P(ly["out"].data_ptr()),
+                                              P(dws.data_ptr()), dws.numel(), sp)
+        ms_s, _ = time_graph(dec, 20, 3, _D(), stream)
+        ms_d, _ = time_graph(den, 10, 2, _D(), stream)
+        us_s, us_d = ms_s / 20 / L * 1e3, ms_d / 10 / L * 1e3
+        out[name] = {"us_per_layer": round(us_s, 3), "dense_us_per_layer": round(us_d, 3),
+                     "speedup_vs_dense": round(us_d / us_s, 3),
+                     "gbs": round(ledger.layer_bytes_alg(cfg) / (us_s * 1e-6) / 1e9, 1)}
+        del layers, ws, dws
+        torch.cuda.empty_cache()
+    return out
+
+
+# ------------------------------------------------------ the oracle (CPU)
+def oracle_sample(cfg: synth.Config, n_seq: int, seed: int):
+    """Host inputs for n_seq sequences of cfg (all H_kv units each)."""
+    import oracle
+    sc = cfg.with_(B=n_seq)
+    lay = synth.make_layer(sc, seed, device="cpu")
+    q, K, V = lay.q.float().numpy(), lay.K.float().numpy(), lay.V.float().numpy()
+    C = lay.C_plant.numpy()
+    import numpy as np
+    L = np.empty((sc.B, sc.Hkv, sc.S, sc.r), np.float32)
+    for b in range(sc.B):
+        for h in range(sc.Hkv):
+            L[b, h] = oracle.label_gather(K[b, h], C[h])
+    return sc, q, K, V, L, C, lay.seq_lens.numpy()
+
+
+def cpu_baseline(cfg: synth.Config, budget_s: float = 12.0, nthreads=None):
+    """The oracle as it stands, on this host's cores, on a bounded sample of the
+    same workload: whole sequences (all KV heads) of cfg, as many as fit the
+    time budget (pilot-timed)."""
+    import oracle
+    nthreads = nthreads or os.cpu_count() or 1
+    sc, q, K, V, L, C, sl = oracle_sample(cfg, 1, seed=cfg.seed_base + 777)
+    t = time.perf_counter()
+    oracle.decode_batch(q, K, V, L, C, sl, cfg.k, nthreads=nthreads)
+    pilot = time.perf_counter() - t
+    reps = max(1, int(budget_s / max(pilot, 1e-3)))
+    t = time.perf_counter()
+    for _ in range(reps):
+        oracle.decode_batch(q, K, V, L, C, sl, cfg.k, nthreads=nthreads)
+    dt = time.perf_counter() - t
+    units = sc.units * reps
+    bytes_ = units * ledger.unit_bytes_alg(cfg.S, cfg.d, cfg.r, cfg.k, cfg.elem)
+    return {"value": round(bytes_ / dt / 1e9, 4), "unit": "GB/s", "cores": nthreads, "kind": "oracle",
+            "sample": f"{reps} x 1 sequence ({sc.units} units of {cfg.name}, S={cfg.S}, k={cfg.k}) "
+                      f"Algorithm 1 in plain fp32 C, {dt:.1f} s",
+            "us_per_unit": round(dt / units * 1e6, 1)}
+
+
+def run_reference(args, dist):
+    import oracle
+    full = synth.CONFIGS[args.config]
+    nthreads = os.cpu_count() or 1
+    sc, q, K, V, L, C, sl = oracle_sample(full, 1, seed=full.seed_base + 777)
+    t = time.perf_counter()
+    oracle.decode_batch(q, K, V, L, C, sl, full.k, nthreads=nthreads)
+    pilot = time.perf_counter() - t
+    reps = max(1, int(2.0 / max(pilot, 1e-3)))     # ~2 s of CPU work per step
+    for _ in range(args.warmup):
+        for _ in range(reps):
+            oracle.decode_batch(q, K, V, L, C, sl, full.k, nthreads=nthreads)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        for _ in range(reps):
+            oracle.decode_batch(q, K, V, L, C, sl, full.k, nthreads=nthreads)
+    dt = time.perf_counter() - t
+    units = sc.units * reps * args.steps
+    value = units * ledger.unit_bytes_alg(full.S, full.d, full.r, full.k, full.elem) / dt / 1e9
+    ms_step = dt / args.steps * 1e3
+    sample = f"{reps} x 1 sequence ({sc.units} units) of {full.name} per step, plain fp32 C oracle"
+    return {"metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": full.dtype, "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{full.name}: B={full.B} Hq={full.Hq} Hkv={full.Hkv} d={full.d} S={full.S} "
+                                   f"r={full.r} k={full.k} {full.dtype}", "sample_per_step": sample},
+            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": nthreads, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    dist = Dist()
+    if args.impl == "reference":
+        if dist.rank != 0:
+            return 0
+        print(json.dumps(run_reference(args, dist)), flush=True)
+        return 0
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py (ours) needs a CUDA device; there is no CPU fallback")
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    dist.init("nccl")
+    res = run_ours(args, dist)
+    if dist.rank == 0:
+        print(json.dumps(res), flush=True)
+    dist.done()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

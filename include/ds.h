@@ -1,0 +1,156 @@
+/*
+ * ds.h -- C ABI of libds.so: the Double Sparsity decode-attention hot path
+ * (arXiv 2408.07092) as hand-written CUDA for NVIDIA B200 (sm_100a).
+ *
+ * Citations: "P:n" is line n of the paper text (/root/reference/PAPER.md,
+ * v1 LaTeX), with the section / algorithm line it falls in.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Ownership: every buffer is allocated by the caller (e.g. a torch
+ *    tensor's data_ptr()).  The library never allocates, frees or retains
+ *    a pointer past the call, and keeps no mutable global state (only a
+ *    once-initialised kernel-attribute setup).  Calls are thread-safe.
+ *  - Asynchrony: every call only validates on the host and enqueues
+ *    kernels on the caller's stream; results are visible in stream order.
+ *    All calls are legal inside CUDA-graph capture.
+ *  - Pointers are device pointers unless stated otherwise (host-mapped
+ *    pinned memory is a valid device pointer).  All tensors are dense,
+ *    row-major, 16-byte aligned.
+ *  - Errors: a ds_status return code, never an exception or exit().
+ *    Host-checkable preconditions (shapes, dtypes, alignment, ranges of
+ *    scalars, workspace size) return DS_ERR_INVALID_ARGUMENT /
+ *    DS_ERR_UNSUPPORTED / DS_ERR_WORKSPACE_TOO_SMALL before anything is
+ *    enqueued.  A failed launch returns DS_ERR_CUDA.  Data-dependent
+ *    preconditions that live in device memory (channel ids < head_dim and
+ *    ascending, block-table entries < num_pages, seq_lens <= max_seq_len,
+ *    append positions in range, finite inputs) are the caller's contract
+ *    and are not checked: violating them is undefined behaviour.
+ *  - dtype: q, K, V, the label cache and out share one element type.  The
+ *    label cache has the same 16-bit (or 32-bit) type as K, so
+ *    "label == channel gather of K" holds bit for bit (DESIGN reading R8).
+ *  - Supported shapes: head_dim in {64, 128}; G = num_q_heads /
+ *    num_kv_heads in {1, 2, 4, 8}; 1 <= r <= head_dim; page_size >= 1.
+ *    Others return DS_ERR_UNSUPPORTED.
+ */
+#ifndef DS_H_
+#define DS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DS_OK = 0,
+  DS_ERR_INVALID_ARGUMENT = 1,
+  DS_ERR_UNSUPPORTED = 2,
+  DS_ERR_GQA_INCOMPATIBLE = 3, /* k-outlier calibration with GQA, P:298 (Table 3) */
+  DS_ERR_WORKSPACE_TOO_SMALL = 4,
+  DS_ERR_CUDA = 5
+} ds_status;
+
+typedef enum { DS_FP16 = 0, DS_BF16 = 1, DS_FP32 = 2 } ds_dtype;
+
+/* Outlier-channel modes of Table 3: qk (default), q, k, random. */
+typedef enum { DS_CALIB_QK = 0, DS_CALIB_Q = 1, DS_CALIB_K = 2, DS_CALIB_RANDOM = 3 } ds_calib_mode;
+
+/* One layer's cache (the full KV cache is kept; plus the label
+ * cache).  All pointers are device pointers.
+ *   k_pool, v_pool : [num_pages][num_kv_heads][page_size][head_dim]
+ *                    token t of sequence b, head h lives in page
+ *                    block_table[b][t / page_size], slot t % page_size.
+ *   block_table    : int32 [batch][max_pages_per_seq]
+ *   seq_lens       : int32 [batch]; attention reads tokens t < seq_lens[b]
+ *                    (the caller appends the current token first, reading R10)
+ *   label          : [batch][num_kv_heads][max_seq_len][r]   K_label
+ *   channel_idx    : int32 [num_kv_heads][r] = C, ascending, distinct.   */
+typedef struct {
+  int32_t batch, num_q_heads, num_kv_heads, head_dim;
+  int32_t page_size, num_pages, max_pages_per_seq, max_seq_len, r;
+  ds_dtype dtype;
+  void *k_pool, *v_pool;
+  const int32_t *block_table;
+  const int32_t *seq_lens;
+  void *label;
+  const int32_t *channel_idx;
+} ds_cache;
+
+/* Human-readable name of a status code (static string, never NULL). */
+const char *ds_status_string(ds_status s);
+
+/* Library version string, e.g. "ds-b200 0.1 sm_100a". */
+const char *ds_version(void);
+
+/* Offline calibration, Sec. 4.1: A = sum_i S_i, S_i = Q_i*K_i;
+ * pick the r channels with the largest aggregated |S_i| per KV head
+ * (readings R4, R5: per KV head, group's q heads summed; fp64 sums of
+ * |Q| and |K| over the n calibration samples, importance = product for
+ * qk mode, the |Q| sum for q mode, the |K| sum for k mode; random mode is
+ * a seeded splitmix64 Fisher-Yates draw).  Ties go to the lower channel;
+ * output is ascending.
+ *   q_calib [n][num_q_heads][head_dim], k_calib [n][num_kv_heads][head_dim]
+ *   channel_idx_out int32 [num_kv_heads][r] (device).
+ * Errors: DS_ERR_GQA_INCOMPATIBLE for k mode with num_q_heads != num_kv_heads. */
+ds_status ds_calibrate_channels(const void *q_calib, const void *k_calib, int32_t n,
+                                int32_t num_q_heads, int32_t num_kv_heads, int32_t head_dim,
+                                ds_dtype dtype, ds_calib_mode mode, int32_t r, uint64_t seed,
+                                int32_t *channel_idx_out, cudaStream_t stream);
+
+/* Label-cache append, Sec. 4.2: "During the prefilling stage, all
+ * heavy channel values from the Key cache are stored in the label cache;
+ * in the decoding phase, only the heavy channel values of new tokens are
+ * added."  For every b < batch, i < n_new, h: token p = positions[b] + i
+ * gets K/V rows k_new[b][i][h][:], v_new[b][i][h][:] written into its
+ * page slot and label[b][h][p][j] = k_new[b][i][h][C[h][j]] (a bit copy).
+ *   k_new, v_new : [batch][n_new][num_kv_heads][head_dim]
+ *   positions    : int32 [batch] (device), first write position per
+ *                  sequence; p < max_seq_len and its page must be mapped.
+ * Does not modify seq_lens (the caller owns it). */
+ds_status ds_append_kv(const ds_cache *c, const void *k_new, const void *v_new,
+                       const int32_t *positions, int32_t n_new, cudaStream_t stream);
+
+/* Bytes of workspace ds_decode_attention needs for this cache and k
+ * (0 on invalid arguments). */
+size_t ds_decode_workspace_size(const ds_cache *c, int32_t k);
+
+/* Algorithm 1 "Double Sparsity Decode", one decode query per
+ * sequence, every (b, KV head) unit independently:
+ *   1  Q_label <- Q_[C]                (group-summed for GQA, reading R3)
+ *   2  s_hat   <- Q_label . K_label^T  (fp32 fma chain over j ascending,
+ *                                       no 1/sqrt(d), reading R2)
+ *   3  i       <- argtopk(s_hat, k_eff), k_eff = min(k, seq_lens[b]);
+ *                 ties to the lower index, ascending (reading R6)
+ *   4  s       <- softmax(Q . K_[i,:]^T / sqrt(d_h))   (fp32)
+ *   5  y       <- s . V_[i,:]          -> out, rounded to dtype (RNE)
+ *   q   : [batch][num_q_heads][head_dim]
+ *   out : [batch][num_q_heads][head_dim]
+ *   topk_idx_out : nullable int32 [batch][num_kv_heads][k]; positions
+ *                  >= k_eff are set to -1.
+ *   workspace    : >= ds_decode_workspace_size(c, k) bytes of device memory
+ *                  (contents ignored on entry, clobbered).
+ * Errors: DS_ERR_INVALID_ARGUMENT if k < 1 or k > max_seq_len. A sequence
+ * with seq_lens[b] == 0 yields out = 0. */
+ds_status ds_decode_attention(const ds_cache *c, const void *q, int32_t k, void *out,
+                              int32_t *topk_idx_out, void *workspace, size_t workspace_bytes,
+                              cudaStream_t stream);
+
+/* Lines 1-2 of Algorithm 1 only, for diagnostics and tests:
+ * scores_out fp32 [batch][num_kv_heads][max_seq_len]; entries t >=
+ * seq_lens[b] are left untouched.  Same arithmetic as ds_decode_attention. */
+ds_status ds_approx_scores(const ds_cache *c, const void *q, float *scores_out,
+                           cudaStream_t stream);
+
+/* Dense decode attention baseline on the same paged layout, Sec. 2.1
+ * (P:43): y = softmax(q K^T / sqrt(d_h)) V over every token t < seq_lens[b]. */
+size_t ds_dense_workspace_size(const ds_cache *c);
+ds_status ds_dense_decode_attention(const ds_cache *c, const void *q, void *out, void *workspace,
+                                    size_t workspace_bytes, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DS_H_ */

@@ -1,0 +1,237 @@
+"""Double Sparsity decode attention (arXiv 2408.07092), native on NVIDIA B200.
+
+Thin Python binding over the C ABI of ``libds.so`` (``include/ds.h``): the
+functions below have the C names and only marshal arguments (torch tensors
+-> device pointers, the current CUDA stream).  Every step of the method runs
+in the sm_100a kernels under ``csrc/``.  There is no CPU fallback: if the
+library is missing or the device is not a CUDA device, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libds.so")
+
+DS_OK, DS_ERR_INVALID_ARGUMENT, DS_ERR_UNSUPPORTED, DS_ERR_GQA_INCOMPATIBLE, \
+    DS_ERR_WORKSPACE_TOO_SMALL, DS_ERR_CUDA = range(6)
+DS_FP16, DS_BF16, DS_FP32 = 0, 1, 2
+DS_CALIB_QK, DS_CALIB_Q, DS_CALIB_K, DS_CALIB_RANDOM = 0, 1, 2, 3
+
+_DT = {torch.float16: DS_FP16, torch.bfloat16: DS_BF16, torch.float32: DS_FP32}
+
+
+class DsError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {ds_status_string(status)}")
+        self.status = status
+
+
+class GqaIncompatible(DsError):
+    pass
+
+
+class ds_cache(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("num_q_heads", ctypes.c_int32),
+                ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("page_size", ctypes.c_int32), ("num_pages", ctypes.c_int32),
+                ("max_pages_per_seq", ctypes.c_int32), ("max_seq_len", ctypes.c_int32),
+                ("r", ctypes.c_int32), ("dtype", ctypes.c_int),
+                ("k_pool", ctypes.c_void_p), ("v_pool", ctypes.c_void_p),
+                ("block_table", ctypes.c_void_p), ("seq_lens", ctypes.c_void_p),
+                ("label", ctypes.c_void_p), ("channel_idx", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libds.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2408_07092_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
+        C = ctypes.POINTER(ds_cache)
+        L.ds_status_string.argtypes = [ctypes.c_int]
+        L.ds_status_string.restype = ctypes.c_char_p
+        L.ds_version.restype = ctypes.c_char_p
+        L.ds_calibrate_channels.argtypes = [P, P, I32, I32, I32, I32, ctypes.c_int, ctypes.c_int, I32,
+                                            ctypes.c_uint64, P, P]
+        L.ds_append_kv.argtypes = [C, P, P, P, I32, P]
+        L.ds_decode_workspace_size.argtypes = [C, I32]
+        L.ds_decode_workspace_size.restype = SZ
+        L.ds_decode_attention.argtypes = [C, P, I32, P, P, P, SZ, P]
+        L.ds_approx_scores.argtypes = [C, P, P, P]
+        L.ds_dense_workspace_size.argtypes = [C]
+        L.ds_dense_workspace_size.restype = SZ
+        L.ds_dense_decode_attention.argtypes = [C, P, P, P, SZ, P]
+        for f in ("ds_calibrate_channels", "ds_append_kv", "ds_decode_attention", "ds_approx_scores",
+                  "ds_dense_decode_attention"):
+            getattr(L, f).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+EXPORTS = ("ds_status_string", "ds_version", "ds_calibrate_channels", "ds_append_kv",
+           "ds_decode_workspace_size", "ds_decode_attention", "ds_approx_scores",
+           "ds_dense_workspace_size", "ds_dense_decode_attention")
+
+
+def ds_status_string(s: int) -> str:
+    return lib().ds_status_string(s).decode()
+
+
+def ds_version() -> str:
+    return lib().ds_version().decode()
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libds takes device tensors (no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError("libds takes contiguous tensors")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check(status: int, what: str):
+    if status == DS_ERR_GQA_INCOMPATIBLE:
+        raise GqaIncompatible(status, what)
+    if status != DS_OK:
+        raise DsError(status, what)
+
+
+@dataclass
+class LayerCache:
+    """Device buffers of one layer's cache (the ds_cache struct of ds.h).
+    Allocation is plumbing (torch); contents are written by ds_append_kv."""
+    batch: int
+    num_q_heads: int
+    num_kv_heads: int
+    head_dim: int
+    page_size: int
+    max_seq_len: int
+    r: int
+    dtype: torch.dtype
+    k_pool: torch.Tensor
+    v_pool: torch.Tensor
+    block_table: torch.Tensor
+    seq_lens: torch.Tensor
+    label: torch.Tensor
+    channel_idx: torch.Tensor
+
+    @staticmethod
+    def allocate(batch, num_q_heads, num_kv_heads, head_dim, max_seq_len, r, dtype, block_table,
+                 num_pages=None, page_size=16, device="cuda", channel_idx=None):
+        bt = torch.as_tensor(block_table, dtype=torch.int32).to(device).contiguous()
+        npages = int(num_pages if num_pages is not None else int(bt.max()) + 1)
+        pool = (npages, num_kv_heads, page_size, head_dim)
+        return LayerCache(
+            batch, num_q_heads, num_kv_heads, head_dim, page_size, max_seq_len, r, dtype,
+            torch.empty(pool, dtype=dtype, device=device), torch.empty(pool, dtype=dtype, device=device),
+            bt, torch.zeros(batch, dtype=torch.int32, device=device),
+            torch.empty((batch, num_kv_heads, max_seq_len, r), dtype=dtype, device=device),
+            (torch.as_tensor(channel_idx, dtype=torch.int32).to(device).contiguous() if channel_idx is not None
+             else torch.zeros((num_kv_heads, r), dtype=torch.int32, device=device)))
+
+    @property
+    def num_pages(self):
+        return self.k_pool.shape[0]
+
+    def struct(self) -> ds_cache:
+        return ds_cache(self.batch, self.num_q_heads, self.num_kv_heads, self.head_dim, self.page_size,
+                        self.num_pages, self.block_table.shape[1], self.max_seq_len, self.r,
+                        _DT[self.dtype], _ptr(self.k_pool), _ptr(self.v_pool), _ptr(self.block_table),
+                        _ptr(self.seq_lens), _ptr(self.label), _ptr(self.channel_idx))
+
+
+def ds_calibrate_channels(q_calib, k_calib, num_kv_heads, r, mode=DS_CALIB_QK, seed=0, out=None, stream=None):
+    """Offline channel calibration. q_calib [n][Hq][d], k_calib [n][Hkv][d] -> int32 [Hkv][r]."""
+    n, hq, d = q_calib.shape
+    if out is None:
+        out = torch.empty((num_kv_heads, r), dtype=torch.int32, device=q_calib.device)
+    st = lib().ds_calibrate_channels(_ptr(q_calib), _ptr(k_calib), n, hq, num_kv_heads, d, _DT[q_calib.dtype],
+                                     mode, r, ctypes.c_uint64(seed), _ptr(out), _stream(stream))
+    _check(st, "ds_calibrate_channels")
+    return out
+
+
+def ds_append_kv(cache: LayerCache, k_new, v_new, positions, stream=None, cs=None):
+    """Write K/V rows + label rows of n_new tokens per sequence. k_new [B][n_new][Hkv][d]."""
+    cs = cs if cs is not None else cache.struct()
+    st = lib().ds_append_kv(ctypes.byref(cs), _ptr(k_new), _ptr(v_new), _ptr(positions), k_new.shape[1],
+                            _stream(stream))
+    _check(st, "ds_append_kv")
+
+
+def ds_decode_workspace_size(cache: LayerCache, k: int) -> int:
+    return lib().ds_decode_workspace_size(ctypes.byref(cache.struct()), k)
+
+
+def ds_dense_workspace_size(cache: LayerCache) -> int:
+    return lib().ds_dense_workspace_size(ctypes.byref(cache.struct()))
+
+
+def workspace(nbytes: int, device="cuda") -> torch.Tensor:
+    return torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+
+
+def ds_decode_attention(cache: LayerCache, q, k, out=None, topk_idx_out=None, ws=None, stream=None, cs=None):
+    """Algorithm 1. q [B][Hq][d] -> out [B][Hq][d]."""
+    cs = cs if cs is not None else cache.struct()
+    if out is None:
+        out = torch.empty_like(q)
+    if ws is None:
+        ws = workspace(lib().ds_decode_workspace_size(ctypes.byref(cs), k), q.device)
+    st = lib().ds_decode_attention(ctypes.byref(cs), _ptr(q), k, _ptr(out), _ptr(topk_idx_out), _ptr(ws),
+                                   ws.numel(), _stream(stream))
+    _check(st, "ds_decode_attention")
+    return out
+
+
+def ds_approx_scores(cache: LayerCache, q, out=None, stream=None):
+    """Lines 1-2 of Alg. 1 only: fp32 [B][Hkv][max_seq_len]."""
+    if out is None:
+        out = torch.full((cache.batch, cache.num_kv_heads, cache.max_seq_len), float("nan"),
+                         dtype=torch.float32, device=q.device)
+    st = lib().ds_approx_scores(ctypes.byref(cache.struct()), _ptr(q), _ptr(out), _stream(stream))
+    _check(st, "ds_approx_scores")
+    return out
+
+
+def ds_dense_decode_attention(cache: LayerCache, q, out=None, ws=None, stream=None, cs=None):
+    """Dense decode baseline on the same paged layout."""
+    cs = cs if cs is not None else cache.struct()
+    if out is None:
+        out = torch.empty_like(q)
+    if ws is None:
+        ws = workspace(lib().ds_dense_workspace_size(ctypes.byref(cs)), q.device)
+    st = lib().ds_dense_decode_attention(ctypes.byref(cs), _ptr(q), _ptr(out), _ptr(ws), ws.numel(),
+                                         _stream(stream))
+    _check(st, "ds_dense_decode_attention")
+    return out
+
+
+def prefill(cache: LayerCache, K, V, seq_lens, stream=None):
+    """Fill a cache from dense K, V [B][Hkv][S][d] through ds_append_kv (a0);
+    sets seq_lens.  (Layout transpose to the append's [B][n][Hkv][d] is a
+    torch copy: plumbing, not method arithmetic.)"""
+    B = K.shape[0]
+    kn = K.transpose(1, 2).contiguous()
+    vn = V.transpose(1, 2).contiguous()
+    pos = torch.zeros(B, dtype=torch.int32, device=K.device)
+    ds_append_kv(cache, kn, vn, pos, stream=stream)
+    cache.seq_lens.copy_(torch.as_tensor(seq_lens, dtype=torch.int32))

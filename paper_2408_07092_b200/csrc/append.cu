@@ -1,0 +1,63 @@
+// append.cu -- a0: KV + label-cache append (Sec. 4.2).
+//
+// One warp per (b, new token i, KV head h): 16-byte vector copies of the K
+// and V rows into their page slot, then the r label channels
+// label[b][h][p][j] = k_new[b][i][h][C[h][j]] as a bit copy of the same
+// element type.  Bytes per unit and token: 2*d*e (KV) + r*e (label).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "ds_common.cuh"
+#include "ds_internal.h"
+
+namespace ds {
+
+template <typename T>
+__global__ void __launch_bounds__(128) append_kernel(CacheView c, const T *__restrict__ k_new,
+                                                     const T *__restrict__ v_new,
+                                                     const int32_t *__restrict__ positions,
+                                                     int n_new) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.y;
+  const int row = blockIdx.x * 4 + warp;  // over (i, h)
+  if (row >= n_new * c.Hkv) return;
+  const int i = row / c.Hkv, h = row - i * c.Hkv;
+  const int p = positions[b] + i;
+  const int page = c.block_table[(size_t)b * c.maxp + p / c.P];
+  const size_t dst = (((size_t)page * c.Hkv + h) * c.P + (p % c.P)) * c.D;
+  const size_t src = (((size_t)b * n_new + i) * c.Hkv + h) * (size_t)c.D;
+  const int nvec = c.D * (int)sizeof(T) / 16;
+  const uint4 *ks = reinterpret_cast<const uint4 *>(k_new + src);
+  const uint4 *vs = reinterpret_cast<const uint4 *>(v_new + src);
+  uint4 *kd = reinterpret_cast<uint4 *>((T *)c.k_pool + dst);
+  uint4 *vd = reinterpret_cast<uint4 *>((T *)c.v_pool + dst);
+  for (int v = lane; v < nvec; v += 32) {
+    kd[v] = ks[v];
+    vd[v] = vs[v];
+  }
+  T *lab = (T *)c.label + (((size_t)b * c.Hkv + h) * c.Smax + p) * c.r;
+  const int32_t *C = c.C + (size_t)h * c.r;
+  for (int j = lane; j < c.r; j += 32) lab[j] = k_new[src + C[j]];
+}
+
+cudaError_t launch_append(const ds_cache *cc, const void *k_new, const void *v_new,
+                          const int32_t *positions, int n_new, cudaStream_t st) {
+  CacheView c = make_view(cc);
+  dim3 grid((n_new * c.Hkv + 3) / 4, c.B);
+  switch (cc->dtype) {
+    case DS_BF16:
+      append_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(c, (const __nv_bfloat16 *)k_new,
+                                                         (const __nv_bfloat16 *)v_new, positions, n_new);
+      break;
+    case DS_FP16:
+      append_kernel<__half><<<grid, 128, 0, st>>>(c, (const __half *)k_new, (const __half *)v_new,
+                                                  positions, n_new);
+      break;
+    default:
+      append_kernel<float><<<grid, 128, 0, st>>>(c, (const float *)k_new, (const float *)v_new, positions,
+                                                 n_new);
+  }
+  return cudaPeekAtLastError();
+}
+
+}  // namespace ds

@@ -1,0 +1,86 @@
+"""Shared helpers for the GPU parity tests: build a device cache from synth
+inputs through the product path (ds_append_kv), run the oracle on the same
+values copied to the host, and apply the tolerance rules of DESIGN.md
+(readings R13, R14).  Expected values come only from oracle/."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle
+import paper_2408_07092_b200 as ds
+import synth
+
+TOL = {"fp32": (1e-5, 1e-4), "fp16": (2e-3, 1e-2), "bf16": (2e-3, 1e-2)}   # (atol, rtol)
+
+
+def build_cache(cfg: synth.Config, seed=None, structure="iid", seq_lens=None, C=None, identity_pages=False,
+                device="cuda"):
+    lay = synth.make_layer(cfg, seed, device=device, structure=structure, seq_lens=seq_lens,
+                           identity_pages=identity_pages)
+    C = lay.C_plant if C is None else torch.as_tensor(C, dtype=torch.int32)
+    cache = ds.LayerCache.allocate(cfg.B, cfg.Hq, cfg.Hkv, cfg.d, cfg.S, cfg.r, synth.DTYPES[cfg.dtype],
+                                   lay.block_table, num_pages=lay.num_pages, page_size=cfg.page_size,
+                                   device=device, channel_idx=C)
+    ds.prefill(cache, lay.K, lay.V, lay.seq_lens)
+    return lay, cache, C
+
+
+def unit_host(lay, b, h):
+    """Dense host fp32 copies of one unit (widening is exact)."""
+    S = int(lay.seq_lens[b])
+    G = lay.cfg.G
+    q = lay.q[b, h * G:(h + 1) * G].float().cpu().numpy()
+    K = lay.K[b, h, :S].float().cpu().numpy()
+    V = lay.V[b, h, :S].float().cpu().numpy()
+    return q, K, V
+
+
+def check_selection(idx_gpu, idx_ref, shat_ref, tau, keff):
+    """R13: index sets bit-exact except tokens in the symmetric difference
+    whose oracle score lies within 1e-3*max(1,|tau|) of the k-th score."""
+    g = np.asarray(idx_gpu)
+    assert np.all(g[keff:] == -1), "positions >= k_eff must be -1"
+    g = g[:keff]
+    assert np.all(np.diff(g) > 0), "indices must be strictly ascending"
+    assert g.min() >= 0 and g.max() < len(shat_ref)
+    sym = set(g.tolist()) ^ set(np.asarray(idx_ref).tolist())
+    band = 1e-3 * max(1.0, abs(tau))
+    bad = [t for t in sym if abs(float(shat_ref[t]) - tau) > band]
+    assert not bad, f"{len(bad)} tokens differ outside the tau band (tau={tau}), e.g. {bad[:5]}"
+    return len(sym)
+
+
+def check_output(y_gpu, y_ref, dtype):
+    atol, rtol = TOL[dtype]
+    y_gpu = np.asarray(y_gpu, np.float64)
+    y_ref = np.asarray(y_ref, np.float64)
+    err = np.abs(y_gpu - y_ref)
+    lim = atol + rtol * np.abs(y_ref)
+    assert np.all(err <= lim), f"max excess {np.max(err - lim):.3g}, max abs err {err.max():.3g}"
+    return float(err.max())
+
+
+def check_units(lay, cache, C, k, units, y_gpu, idx_gpu):
+    """Run the oracle on the listed (b, h) units and check selection + output."""
+    cfg = lay.cfg
+    G = cfg.G
+    Ch = C.cpu().numpy()
+    y_gpu = y_gpu.float().cpu().numpy()
+    idx_gpu = idx_gpu.cpu().numpy()
+    nsym = 0
+    for b, h in units:
+        q, K, V = unit_host(lay, b, h)
+        S = K.shape[0]
+        L = oracle.label_gather(K, Ch[h])
+        y_ref, idx_ref, shat, tau = oracle.ds_decode_unit(q, K, V, L, Ch[h], k)
+        keff = min(k, S)
+        nsym += check_selection(idx_gpu[b, h], idx_ref, shat, tau, keff)
+        # attention checked on the GPU's own index set (truncated oracle)
+        sel = idx_gpu[b, h, :keff]
+        for g in range(G):
+            ref = oracle.attend(q[g], K, V, sel) if keff > 0 else np.zeros(cfg.d, np.float32)
+            check_output(y_gpu[b, h * G + g], ref, cfg.dtype)
+            if set(sel.tolist()) == set(idx_ref.tolist()):
+                check_output(y_gpu[b, h * G + g], y_ref[g], cfg.dtype)
+    return nsym
