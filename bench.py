@@ -39,8 +39,8 @@ from paper_2408_07092_b200 import ledger  # noqa: E402
 
 METRIC = "sparse decode-attn µs/layer & HBM GB/s vs dense, S=32K, 1/16 sparsity, 1-8 B200"
 KERNELS_PER_APPEND = 1
-KERNELS_PER_DECODE = 3      # score+select (cluster), split-K attention, combine
-KERNELS_PER_DENSE = 2
+KERNELS_PER_DECODE = 2      # score+select (cluster per unit), split-K attention (cluster per unit)
+KERNELS_PER_DENSE = 1
 
 
 def parse():
@@ -149,7 +149,7 @@ class Clocks:
             return None
         sm = [float(p[1]) for p in rows]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for p in rows for i in range(4) if "Active" in p[5 + i]})
+        reasons = sorted({names[i] for p in rows for i in range(4) if p[5 + i].strip() == "Active"})
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
                 "samples": len(rows), "power_w_max": max(float(p[3]) for p in rows if p[3].replace(".", "").isdigit())
                 if any(p[3].replace(".", "").isdigit() for p in rows) else None}
@@ -189,17 +189,18 @@ def time_graph(fn, steps, warmup, dist, stream):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=stream):
         fn()
-    for _ in range(warmup):
-        g.replay()
-    torch.cuda.synchronize()
-    dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        g.replay()
-    e1.record(stream)
-    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):           # replay() launches on the current stream
+        for _ in range(warmup):
+            g.replay()
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
     dist.barrier()
     return e0.elapsed_time(e1), g
 
@@ -279,7 +280,7 @@ def run_ours(args, dist):
             traffic = None
     res["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                        "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-                       "kernel": "ds_decode_attention launch group (score_select + attn_split + combine)",
+                       "kernel": "ds_decode_attention launch group (score_select_kernel + attn_kernel)",
                        "us_per_launch": round(us_decode, 3), "peak_source": peak_src,
                        "algorithmic_bytes_per_launch": bytes_layer}
     res["gpu_launches"] = args.steps * L * (KERNELS_PER_APPEND + KERNELS_PER_DECODE)

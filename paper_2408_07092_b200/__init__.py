@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libds.so")
+LIB_PATH = os.environ.get("DS_LIB") or os.path.join(_PKG, "libds.so")  # DS_LIB: debug builds only
 
 DS_OK, DS_ERR_INVALID_ARGUMENT, DS_ERR_UNSUPPORTED, DS_ERR_GQA_INCOMPATIBLE, \
     DS_ERR_WORKSPACE_TOO_SMALL, DS_ERR_CUDA = range(6)

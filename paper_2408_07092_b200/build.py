@@ -60,5 +60,21 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
+def build_trace() -> str:
+    """Debug library with per-CTA phase timestamps (-DDS_TRACE), one unity TU."""
+    os.makedirs(BUILD, exist_ok=True)
+    unity = os.path.join(BUILD, "unity_trace.cu")
+    with open(unity, "w") as f:
+        for src in _sources():
+            f.write('#include "%s"\n' % src)
+    out = os.path.join(PKG, "libds_trace.so")
+    subprocess.check_call([NVCC, *ARCH, *[x for x in FLAGS if x not in ("-v", "-Xptxas")], "-DDS_TRACE", "-shared", unity,
+                           "-o", out])
+    return out
+
+
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    if "--trace" in sys.argv:
+        print(build_trace())
+    else:
+        print(build(verbose="-v" in sys.argv))

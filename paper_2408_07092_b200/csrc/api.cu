@@ -33,22 +33,18 @@ CacheView make_view(const ds_cache *c) {
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-Workspace carve_workspace(const ds_cache *c, int k, int nsplit, void *base) {
+Workspace carve_workspace(const ds_cache *c, int k, void *base) {
   const size_t units = (size_t)c->batch * c->num_kv_heads;
-  const int G = c->num_q_heads / c->num_kv_heads;
-  Workspace w;
-  size_t off = 0;
-  const size_t idx_b = align256(units * (size_t)(k > 0 ? k : 0) * sizeof(int32_t));
-  const size_t po_b = align256(units * nsplit * G * (size_t)c->head_dim * sizeof(float));
-  const size_t pm_b = align256(units * nsplit * G * 2 * sizeof(float));
+  const size_t kb = align256(units * (size_t)(k > 0 ? k : 0) * sizeof(int32_t));
+  const size_t keys_b = align256(select_workspace_keys(c));
+  const size_t hist_b = align256(select_workspace_hist(c));
   char *p = (char *)base;
-  w.idx = (int32_t *)(p ? p + off : nullptr);
-  off += idx_b;
-  w.part_o = (float *)(p ? p + off : nullptr);
-  off += po_b;
-  w.part_ml = (float *)(p ? p + off : nullptr);
-  off += pm_b;
-  w.bytes = off;
+  Workspace w;
+  w.keys = (uint32_t *)(p ? p : nullptr);
+  w.part_hist = (uint32_t *)(p ? p + keys_b : nullptr);
+  w.idx = (int32_t *)(p ? p + keys_b + hist_b : nullptr);
+  w.rowid = (int32_t *)(p ? p + keys_b + hist_b + kb : nullptr);
+  w.bytes = keys_b + hist_b + 2 * kb;
   return w;
 }
 
@@ -123,8 +119,18 @@ ds_status ds_append_kv(const ds_cache *c, const void *k_new, const void *v_new, 
 
 size_t ds_decode_workspace_size(const ds_cache *c, int32_t k) {
   if (validate_cache(c) != DS_OK || k < 1 || k > c->max_seq_len) return 0;
-  AttnGeom g = attn_geom(c, k);
-  return carve_workspace(c, k, g.nsplit, nullptr).bytes;
+  return carve_workspace(c, k, nullptr).bytes;
+}
+
+static void fill_attn(AttnParams &ap, const ds_cache *c, const void *q, const int32_t *rowid, int k,
+                      const AttnGeom &ag, void *out) {
+  ap.c = make_view(c);
+  ap.q = q;
+  ap.rowid = rowid;
+  ap.k = k;
+  ap.rows_per_cta = ag.rows_per_cta;
+  ap.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c->head_dim));
+  ap.out = out;
 }
 
 ds_status ds_decode_attention(const ds_cache *c, const void *q, int32_t k, void *out, int32_t *topk_idx_out,
@@ -132,34 +138,32 @@ ds_status ds_decode_attention(const ds_cache *c, const void *q, int32_t k, void 
   ds_status s = validate_cache(c);
   if (s != DS_OK) return s;
   if (k < 1 || k > c->max_seq_len || !q || !out || !aligned16(q) || !aligned16(out)) return DS_ERR_INVALID_ARGUMENT;
-  AttnGeom ag = attn_geom(c, k);
-  Workspace w = carve_workspace(c, k, ag.nsplit, workspace);
-  if (!workspace || workspace_bytes < w.bytes) return DS_ERR_WORKSPACE_TOO_SMALL;
+  Workspace w = carve_workspace(c, k, workspace);
+  if (!workspace || workspace_bytes < w.bytes || !aligned16(workspace)) return DS_ERR_WORKSPACE_TOO_SMALL;
   SelectGeom sg = select_geom(c);
-  if (sg.smem > 200 * 1024) return DS_ERR_UNSUPPORTED;
+  if (sg.smem > 227 * 1024) return DS_ERR_UNSUPPORTED;
+  AttnGeom ag = attn_geom(c, k);
+  if (ag.nsplit < 1) return DS_ERR_UNSUPPORTED;
+  ScoreParams sc;
+  sc.c = make_view(c);
+  sc.q = q;
+  sc.keys = w.keys;
+  sc.part_hist = w.part_hist;
+  sc.scores = nullptr;
+  sc.chunk = sg.chunk;
+  if (launch_score(c, sc, sg, stream) != cudaSuccess) return DS_ERR_CUDA;
   SelectParams sp;
-  sp.c = make_view(c);
-  sp.q = q;
+  sp.c = sc.c;
   sp.k = k;
+  sp.keys = w.keys;
+  sp.part_hist = w.part_hist;
+  sp.chunk = sg.chunk;
   sp.idx = topk_idx_out ? topk_idx_out : w.idx;
-  sp.scores = nullptr;
-  sp.cap = sg.cap;
-  cudaError_t e = launch_select(c, sp, sg, stream);
-  if (e != cudaSuccess) return DS_ERR_CUDA;
+  sp.rowid = w.rowid;
+  if (launch_select(c, sp, sg, stream) != cudaSuccess) return DS_ERR_CUDA;
   AttnParams ap;
-  ap.c = sp.c;
-  ap.q = q;
-  ap.idx = sp.idx;
-  ap.k = k;
-  ap.rows_per_cta = ag.rows_per_cta;
-  ap.nsplit = ag.nsplit;
-  ap.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c->head_dim));
-  ap.part_o = w.part_o;
-  ap.part_ml = w.part_ml;
-  ap.out = out;
-  e = launch_attn(c, ap, ag, stream);
-  if (e != cudaSuccess) return DS_ERR_CUDA;
-  return cuda_status(launch_combine(c, ap, stream));
+  fill_attn(ap, c, q, w.rowid, k, ag, out);
+  return cuda_status(launch_attn(c, ap, ag, stream));
 }
 
 ds_status ds_approx_scores(const ds_cache *c, const void *q, float *scores_out, cudaStream_t stream) {
@@ -167,44 +171,33 @@ ds_status ds_approx_scores(const ds_cache *c, const void *q, float *scores_out, 
   if (s != DS_OK) return s;
   if (!q || !scores_out || !aligned16(q)) return DS_ERR_INVALID_ARGUMENT;
   SelectGeom sg = select_geom(c);
-  SelectParams sp;
-  sp.c = make_view(c);
-  sp.q = q;
-  sp.k = 1;
-  sp.idx = nullptr;
-  sp.scores = scores_out;
-  sp.cap = sg.cap;
-  return cuda_status(launch_select(c, sp, sg, stream));
+  ScoreParams sc;
+  sc.c = make_view(c);
+  sc.q = q;
+  sc.keys = nullptr;
+  sc.part_hist = nullptr;
+  sc.scores = scores_out;
+  sc.chunk = sg.chunk;
+  return cuda_status(launch_score(c, sc, sg, stream));
 }
 
 size_t ds_dense_workspace_size(const ds_cache *c) {
-  if (validate_cache(c) != DS_OK) return 0;
-  AttnGeom g = attn_geom(c, c->max_seq_len);
-  return carve_workspace(c, 0, g.nsplit, nullptr).bytes;
+  (void)c;
+  return 0;  // the dense path merges its splits on chip
 }
 
 ds_status ds_dense_decode_attention(const ds_cache *c, const void *q, void *out, void *workspace,
                                     size_t workspace_bytes, cudaStream_t stream) {
+  (void)workspace;
+  (void)workspace_bytes;
   ds_status s = validate_cache(c);
   if (s != DS_OK) return s;
   if (!q || !out || !aligned16(q) || !aligned16(out)) return DS_ERR_INVALID_ARGUMENT;
   AttnGeom ag = attn_geom(c, c->max_seq_len);
-  Workspace w = carve_workspace(c, 0, ag.nsplit, workspace);
-  if (!workspace || workspace_bytes < w.bytes) return DS_ERR_WORKSPACE_TOO_SMALL;
+  if (ag.nsplit < 1) return DS_ERR_UNSUPPORTED;
   AttnParams ap;
-  ap.c = make_view(c);
-  ap.q = q;
-  ap.idx = nullptr;
-  ap.k = 0;
-  ap.rows_per_cta = ag.rows_per_cta;
-  ap.nsplit = ag.nsplit;
-  ap.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c->head_dim));
-  ap.part_o = w.part_o;
-  ap.part_ml = w.part_ml;
-  ap.out = out;
-  cudaError_t e = launch_attn(c, ap, ag, stream);
-  if (e != cudaSuccess) return DS_ERR_CUDA;
-  return cuda_status(launch_combine(c, ap, stream));
+  fill_attn(ap, c, q, nullptr, 0, ag, out);
+  return cuda_status(launch_attn(c, ap, ag, stream));
 }
 
 }  // extern "C"

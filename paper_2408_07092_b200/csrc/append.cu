@@ -20,6 +20,8 @@ __global__ void __launch_bounds__(128) append_kernel(CacheView c, const T *__res
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.y;
   const int row = blockIdx.x * 4 + warp;  // over (i, h)
+  pdl_wait();
+  pdl_trigger();
   if (row >= n_new * c.Hkv) return;
   const int i = row / c.Hkv, h = row - i * c.Hkv;
   const int p = positions[b] + i;
@@ -43,21 +45,16 @@ __global__ void __launch_bounds__(128) append_kernel(CacheView c, const T *__res
 cudaError_t launch_append(const ds_cache *cc, const void *k_new, const void *v_new,
                           const int32_t *positions, int n_new, cudaStream_t st) {
   CacheView c = make_view(cc);
-  dim3 grid((n_new * c.Hkv + 3) / 4, c.B);
+  PdlLaunch L(dim3((n_new * c.Hkv + 3) / 4, c.B), dim3(128), 0, st);
   switch (cc->dtype) {
     case DS_BF16:
-      append_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>(c, (const __nv_bfloat16 *)k_new,
-                                                         (const __nv_bfloat16 *)v_new, positions, n_new);
-      break;
+      return L.run(append_kernel<__nv_bfloat16>, c, (const __nv_bfloat16 *)k_new, (const __nv_bfloat16 *)v_new,
+                   positions, n_new);
     case DS_FP16:
-      append_kernel<__half><<<grid, 128, 0, st>>>(c, (const __half *)k_new, (const __half *)v_new,
-                                                  positions, n_new);
-      break;
+      return L.run(append_kernel<__half>, c, (const __half *)k_new, (const __half *)v_new, positions, n_new);
     default:
-      append_kernel<float><<<grid, 128, 0, st>>>(c, (const float *)k_new, (const float *)v_new, positions,
-                                                 n_new);
+      return L.run(append_kernel<float>, c, (const float *)k_new, (const float *)v_new, positions, n_new);
   }
-  return cudaPeekAtLastError();
 }
 
 }  // namespace ds

@@ -76,6 +76,66 @@ template <> struct Mma<__half> {
   }
 };
 
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2,
+                                                  uint32_t &r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+// pack two fp32 into a 16-bit pair (lo = first), round-to-nearest-even
+template <typename T> __device__ __forceinline__ uint32_t pack2(float lo, float hi);
+template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+template <> __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// ------------------------------------------------ mbarrier + TMA bulk copy
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+// 1-D bulk copy global -> shared (async proxy), completion on an mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// ----------------------------------------- programmatic dependent launch
+// Kernels launched with cudaLaunchAttributeProgrammaticStreamSerialization
+// may start while their predecessor drains.  Each kernel only touches data
+// written by its immediate predecessor after pdl_wait(), and triggers its own
+// dependents after that wait, so any pre-wait read is of data written two or
+// more launches earlier (complete by then).  Both are no-ops without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // ------------------------------------------------------------- misc
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -103,3 +163,27 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 }  // namespace ds
+
+// ------------------------------------------------------------ tracing
+// Debug builds only (-DDS_TRACE, libds_trace.so): thread 0 of each CTA
+// stamps %globaltimer at phase boundaries; read back with
+// ds_debug_read_trace().  The product library compiles these to nothing.
+#ifdef DS_TRACE
+namespace ds {
+constexpr int kTraceCtas = 4096, kTraceSlots = 16;
+__device__ unsigned long long g_trace[3][kTraceCtas][kTraceSlots];  // unity trace build: one TU
+}
+#define DS_TRACE_AT(kind, slot)                                                              \
+  do {                                                                                       \
+    const unsigned cta_ = blockIdx.x + blockIdx.y * gridDim.x;                              \
+    if (threadIdx.x == 0 && cta_ < (unsigned)ds::kTraceCtas) {                               \
+      unsigned long long t_;                                                                 \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                \
+      ds::g_trace[kind][cta_][slot] = t_;                                                    \
+    }                                                                                        \
+  } while (0)
+#else
+#define DS_TRACE_AT(kind, slot) \
+  do {                          \
+  } while (0)
+#endif

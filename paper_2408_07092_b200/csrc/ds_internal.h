@@ -16,36 +16,46 @@ struct CacheView {
   const int32_t *C;
 };
 
+// score_kernel: a1 + a2 -> order keys [units][Smax] + partial histograms.
+struct ScoreParams {
+  CacheView c;
+  const void *q;         // [B][Hq][D]
+  uint32_t *keys;        // [units][Smax]
+  uint32_t *part_hist;   // [units][kMaxChunks][2048]
+  float *scores;         // non-null: ds_approx_scores mode (s_hat [units][Smax], no keys)
+  int chunk;             // tokens per score CTA
+};
+
+// select_kernel: a3 -> index list + pool row ids.
 struct SelectParams {
   CacheView c;
-  const void *q;       // [B][Hq][D]
   int k;
-  int32_t *idx;        // [B*Hkv][k]
-  float *scores;       // non-null: ds_approx_scores mode (write s_hat, no select)
-  int cap;             // key capacity per CTA (smem)
+  const uint32_t *keys;
+  const uint32_t *part_hist;
+  int chunk;
+  int32_t *idx;          // [units][k] ascending token indices (-1 past k_eff)
+  int32_t *rowid;        // [units][k] pool row ids of the same tokens
 };
 
 struct AttnParams {
   CacheView c;
   const void *q;            // [B][Hq][D]
-  const int32_t *idx;       // [B*Hkv][k] or nullptr for dense
-  int k;                    // selection size (sparse) ; ignored for dense
-  int rows_per_cta;
-  int nsplit;
+  const int32_t *rowid;     // [units][k] pool rows (sparse) or nullptr (dense: every token)
+  int k;                    // selection size (sparse); ignored for dense
+  int rows_per_cta;         // rows of the index list per CTA (cluster = nsplit CTAs)
   float scale_log2;         // log2(e) / sqrt(D)
-  float *part_o;            // [units][nsplit][G][D]
-  float *part_ml;           // [units][nsplit][G][2]
   void *out;                // [B][Hq][D]
 };
 
 // Launch-geometry decisions (deterministic functions of the cache shape).
 struct SelectGeom {
-  int cl;      // cluster size (CTAs per unit)
-  int cap;     // keys per CTA (multiple of 32)
+  int chunk, nchunks;  // score CTAs per unit
   int threads;
-  size_t smem;
+  size_t smem;         // select_kernel dynamic smem
 };
 SelectGeom select_geom(const ds_cache *c);
+size_t select_workspace_keys(const ds_cache *c);
+size_t select_workspace_hist(const ds_cache *c);
 
 struct AttnGeom {
   int rows_per_cta, nsplit, threads;
@@ -53,13 +63,13 @@ struct AttnGeom {
 };
 AttnGeom attn_geom(const ds_cache *c, int n_rows);
 
-// Workspace layout.
+// Workspace layout: keys | partial histograms | idx | rowid.
 struct Workspace {
-  int32_t *idx;
-  float *part_o, *part_ml;
+  uint32_t *keys, *part_hist;
+  int32_t *idx, *rowid;
   size_t bytes;
 };
-Workspace carve_workspace(const ds_cache *c, int k, int nsplit, void *base);
+Workspace carve_workspace(const ds_cache *c, int k, void *base);
 
 // Kernel launchers (defined in the .cu files); return cudaError_t.
 cudaError_t launch_append(const ds_cache *c, const void *k_new, const void *v_new,
@@ -67,11 +77,32 @@ cudaError_t launch_append(const ds_cache *c, const void *k_new, const void *v_ne
 cudaError_t launch_calibrate(const void *qc, const void *kc, int n, int Hq, int Hkv, int D,
                              ds_dtype dt, int mode, int r, uint64_t seed, int32_t *out,
                              cudaStream_t st);
+cudaError_t launch_score(const ds_cache *c, const ScoreParams &p, const SelectGeom &g, cudaStream_t st);
 cudaError_t launch_select(const ds_cache *c, const SelectParams &p, const SelectGeom &g,
                           cudaStream_t st);
 cudaError_t launch_attn(const ds_cache *c, const AttnParams &p, const AttnGeom &g, cudaStream_t st);
-cudaError_t launch_combine(const ds_cache *c, const AttnParams &p, cudaStream_t st);
 
 CacheView make_view(const ds_cache *c);
+
+// cudaLaunchKernelEx with programmatic stream serialization (PDL): the kernel
+// may start while its predecessor drains (see pdl_wait / pdl_trigger).
+struct PdlLaunch {
+  cudaLaunchConfig_t cfg;
+  cudaLaunchAttribute attr[1];
+  PdlLaunch(dim3 grid, dim3 block, size_t smem, cudaStream_t st) : cfg{} {
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  template <typename... KArgs, typename... Args>
+  cudaError_t run(void (*kern)(KArgs...), Args... args) {
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+  }
+};
 
 }  // namespace ds

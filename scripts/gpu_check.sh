@@ -14,8 +14,8 @@ if [[ $STAGE == all || $STAGE == bench ]]; then
   timeout 900 python bench.py ${BENCH_ARGS:-} > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 fi
 if [[ $STAGE == all || $STAGE == ncu ]]; then
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:ds:: -c 200 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --layers 2 --no-dense --no-e2e --no-cpu-baseline \
     > gpurun_out/ncu_launch.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_launch.log
 fi
-tail -3 gpurun_out/*.log
+for f in gpurun_out/*.log; do echo "== $f"; tail -n 3 $f; done

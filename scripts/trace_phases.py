@@ -1,0 +1,57 @@
+"""Per-CTA phase timeline of the decode kernels (needs libds_trace.so).
+
+usage: DS_LIB=paper_2408_07092_b200/libds_trace.so python scripts/trace_phases.py [config]
+"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2408_07092_b200 as ds
+import synth
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c3"
+cfg = synth.CONFIGS[name]
+lay = synth.make_layer(cfg, cfg.seed_base, device="cuda")
+cache = ds.LayerCache.allocate(cfg.B, cfg.Hq, cfg.Hkv, cfg.d, cfg.S, cfg.r, synth.DTYPES[cfg.dtype], lay.block_table,
+                               num_pages=lay.num_pages, page_size=cfg.page_size, channel_idx=lay.C_plant)
+ds.prefill(cache, lay.K, lay.V, lay.seq_lens)
+del lay.K, lay.V
+L = ds.lib()
+L.ds_debug_read_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+buf = np.zeros((3, 4096, 16), np.uint64)
+for it in range(4):
+    L.ds_debug_clear_trace()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    ds.ds_decode_attention(cache, lay.q, cfg.k)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"iter {it}: decode {e0.elapsed_time(e1) * 1e3:.1f} us (events, incl. launch)")
+L.ds_debug_read_trace(buf.ctypes.data_as(ctypes.c_void_p), buf.nbytes)
+
+
+def report(kind, names):
+    t = buf[kind].astype(np.int64)
+    live = t[:, 0] > 0
+    t = t[live]
+    if len(t) == 0:
+        print("no trace for kind", kind)
+        return
+    t0 = min(buf[k][buf[k][:, 0] > 0][:, 0].min() for k in range(3) if (buf[k][:, 0] > 0).any())
+    print(f"\n{['score', 'select', 'attention'][kind]}: {len(t)} CTAs, span {(t[:, len(names) - 1].max() - t0) / 1e3:.2f} us")
+    for i, n in enumerate(names):
+        v = (t[:, i] - t0) / 1e3
+        print(f"  {n:24s} t(us) min {v.min():7.2f}  p50 {np.median(v):7.2f}  p90 {np.percentile(v, 90):7.2f}  max {v.max():7.2f}")
+    for i in range(1, len(names)):
+        d = (t[:, i] - t[:, i - 1]) / 1e3
+        print(f"  dur {names[i - 1]}->{names[i]:14s} p50 {np.median(d):7.2f} p90 {np.percentile(d, 90):7.2f} max {d.max():7.2f}")
+
+
+report(0, ["start", "done"])
+report(1, ["start", "boundary1", "pass done", "resolved", "compacted"])
+report(2, ["start", "rowids", "loop done", "cluster sync", "merged"])

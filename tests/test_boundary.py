@@ -82,7 +82,7 @@ def test_decode_k_range_and_workspace():
     assert L.ds_decode_attention(ctypes.byref(c), q, 8, o, None, w, 16, None) == ds.DS_ERR_WORKSPACE_TOO_SMALL
     assert L.ds_decode_workspace_size(ctypes.byref(c), 8) > 0
     assert L.ds_decode_workspace_size(ctypes.byref(c), 0) == 0
-    assert L.ds_dense_workspace_size(ctypes.byref(c)) > 0
+    assert L.ds_dense_workspace_size(ctypes.byref(c)) == 0
 
 
 def test_calibration_gqa_k_mode_rejected_on_host():
