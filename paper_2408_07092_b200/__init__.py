@@ -186,7 +186,8 @@ def ds_dense_workspace_size(cache: LayerCache) -> int:
 
 
 def workspace(nbytes: int, device="cuda") -> torch.Tensor:
-    return torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+    """Zero-filled workspace (ds.h: zero before first use; the library leaves it zeroed)."""
+    return torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=device)
 
 
 def ds_decode_attention(cache: LayerCache, q, k, out=None, topk_idx_out=None, ws=None, stream=None, cs=None):

@@ -63,18 +63,55 @@ __device__ __forceinline__ void load_lane(const uint8_t *p, float (&v)[EPL]) {
 }
 
 
+// Sparse path: wait until the unit's selection is published (score_select
+// kernel, possibly still running under PDL); the dense path waits for the
+// predecessor grid.
+__device__ __forceinline__ void wait_inputs(const uint32_t *ready, int unit, int n_sel) {
+  if (ready) {
+    pdl_trigger();
+    if (n_sel > 0) {
+      if (threadIdx.x == 0) {
+        uint32_t v;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ready + unit) : "memory");
+          if (v) break;
+          __nanosleep(128);
+        }
+      }
+      __syncthreads();
+    }
+  } else {
+    pdl_wait();
+    pdl_trigger();
+  }
+}
+
 // Pool row ids of rows [tr0, tr0+tn) of a unit into smem: taken from the
 // select kernel's list (sparse) or resolved through block_table (dense).
 __device__ __forceinline__ void load_rowids(uint32_t *rowids, const int32_t *rid, const int32_t *bt,
                                             const CacheView &c, int h, int tr0, int tn, int nthreads,
                                             int me) {
-  for (int i = me; i < tn; i += nthreads) {
-    if (rid) {
-      rowids[i] = (uint32_t)__ldg(rid + tr0 + i);
-    } else {
-      const int t = tr0 + i;
-      rowids[i] = ((uint32_t)__ldg(bt + t / c.P) * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P + (uint32_t)(t % c.P);
+  // batches of loads into registers before any smem store: the round trips
+  // overlap instead of serialising on the stores
+  constexpr int BU = 8;
+  for (int i0 = me; i0 < tn; i0 += BU * nthreads) {
+    uint32_t v[BU];
+#pragma unroll
+    for (int u = 0; u < BU; ++u) {
+      const int i = i0 + u * nthreads;
+      if (i < tn) {
+        if (rid) {  // written by a kernel that may still be running (PDL): coherent L2 load
+          v[u] = (uint32_t)__ldcg(rid + tr0 + i);
+        } else {
+          const int t = tr0 + i;
+          v[u] = ((uint32_t)__ldg(bt + t / c.P) * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P +
+                 (uint32_t)(t % c.P);
+        }
+      }
     }
+#pragma unroll
+    for (int u = 0; u < BU; ++u)
+      if (i0 + u * nthreads < tn) rowids[i0 + u * nthreads] = v[u];
   }
 }
 
@@ -107,6 +144,7 @@ __device__ __forceinline__ void cluster_merge(cg::cluster_group &cluster, float 
     out[(size_t)g * D + dd] = Elem<T>::from_f(y);
   }
   cluster.sync();  // keep every partial alive until all readers are done
+  if (p.ready && split == 0 && threadIdx.x == 0) p.ready[(size_t)b * p.c.Hkv + h] = 0u;  // consumed
 }
 
 // Merge nw warp partials (wm/wl [nw][G], wo [nw][G][D]) into the CTA partial cm.
@@ -182,8 +220,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_simt_kernel(AttnParams p) {
   const int32_t *bt = c.block_table + (size_t)b * c.maxp;
   const float scale = p.scale_log2;
 
-  pdl_wait();
-  pdl_trigger();
+  wait_inputs(p.ready, unit, n_sel);
   // query operands
   uint32_t bq[(E == 2) ? D / 16 : 1][2];
   if constexpr (E == 2) {
@@ -456,8 +493,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) attn_mma_kernel(AttnParams p) 
 #pragma unroll
   for (int nd = 0; nd < NDT; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.f;
   float m_run = -INFINITY, l_run = 0.f;
-  pdl_wait();  // the row ids come from select_kernel
-  pdl_trigger();
+  wait_inputs(p.ready, unit, n_sel);  // the row ids come from score_select_kernel
 
   // this warp's contiguous share of the CTA's rows, in sub-tiles of kSub
   int per = (row1 - row0 + kMmaWarps - 1) / kMmaWarps;
@@ -602,6 +638,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) attn_mma_kernel(AttnParams p) 
       const int g = i / D;
       out[i] = Elem<T>::from_f(cm[g] == -INFINITY ? 0.f : cm[2 * G + i] / cm[G + g]);
     }
+    if (p.ready && tid == 0) p.ready[unit] = 0u;  // consumed (every warp passed its loads)
   }
   DS_TRACE_AT(2, 4);
 }

@@ -16,31 +16,28 @@ struct CacheView {
   const int32_t *C;
 };
 
-// score_kernel: a1 + a2 -> order keys [units][Smax] + partial histograms.
+// score_select_kernel: a1 + a2 + a3 -> index list + pool row ids per unit.
 struct ScoreParams {
   CacheView c;
   const void *q;         // [B][Hq][D]
-  uint32_t *keys;        // [units][Smax]
-  uint32_t *part_hist;   // [units][kMaxChunks][2048]
-  float *scores;         // non-null: ds_approx_scores mode (s_hat [units][Smax], no keys)
-  int chunk;             // tokens per score CTA
-};
-
-// select_kernel: a3 -> index list + pool row ids.
-struct SelectParams {
-  CacheView c;
   int k;
-  const uint32_t *keys;
-  const uint32_t *part_hist;
-  int chunk;
+  uint2 *cand;           // [units][cand_stride]: (order key, token), chunk segments
+  uint32_t *cand_count;  // [units][kMaxChunks]
+  uint32_t *cand_minmax; // [units][kMaxChunks][2] min / max emitted key
+  uint32_t *counter;     // [units] arrivals of the unit's CTAs (0 between calls)
+  uint32_t *ready;       // [units] selection published (0 between calls)
   int32_t *idx;          // [units][k] ascending token indices (-1 past k_eff)
   int32_t *rowid;        // [units][k] pool row ids of the same tokens
+  float *scores;         // non-null: ds_approx_scores mode (s_hat [units][Smax] only)
+  int chunk;             // tokens per CTA
+  int stage_cap;         // candidates the dynamic smem can stage
 };
 
 struct AttnParams {
   CacheView c;
   const void *q;            // [B][Hq][D]
   const int32_t *rowid;     // [units][k] pool rows (sparse) or nullptr (dense: every token)
+  uint32_t *ready;          // sparse: per-unit selection flags to wait on (reset after use)
   int k;                    // selection size (sparse); ignored for dense
   int rows_per_cta;         // rows of the index list per CTA (cluster = nsplit CTAs)
   float scale_log2;         // log2(e) / sqrt(D)
@@ -51,11 +48,12 @@ struct AttnParams {
 struct SelectGeom {
   int chunk, nchunks;  // score CTAs per unit
   int threads;
-  size_t smem;         // select_kernel dynamic smem
+  size_t score_smem;   // dynamic smem (a chunk's keys / the staged candidates)
+  int stage_cap;
 };
-SelectGeom select_geom(const ds_cache *c);
-size_t select_workspace_keys(const ds_cache *c);
-size_t select_workspace_hist(const ds_cache *c);
+SelectGeom select_geom(const ds_cache *c, int k);
+size_t select_workspace_cand(const ds_cache *c);
+size_t select_workspace_count(const ds_cache *c);
 
 struct AttnGeom {
   int rows_per_cta, nsplit, threads;
@@ -63,9 +61,10 @@ struct AttnGeom {
 };
 AttnGeom attn_geom(const ds_cache *c, int n_rows);
 
-// Workspace layout: keys | partial histograms | idx | rowid.
+// Workspace layout: candidates | candidate counts | counters | ready flags | idx | rowid.
 struct Workspace {
-  uint32_t *keys, *part_hist;
+  uint2 *cand;
+  uint32_t *cand_count, *cand_minmax, *counter, *ready;
   int32_t *idx, *rowid;
   size_t bytes;
 };
@@ -78,8 +77,6 @@ cudaError_t launch_calibrate(const void *qc, const void *kc, int n, int Hq, int 
                              ds_dtype dt, int mode, int r, uint64_t seed, int32_t *out,
                              cudaStream_t st);
 cudaError_t launch_score(const ds_cache *c, const ScoreParams &p, const SelectGeom &g, cudaStream_t st);
-cudaError_t launch_select(const ds_cache *c, const SelectParams &p, const SelectGeom &g,
-                          cudaStream_t st);
 cudaError_t launch_attn(const ds_cache *c, const AttnParams &p, const AttnGeom &g, cudaStream_t st);
 
 CacheView make_view(const ds_cache *c);

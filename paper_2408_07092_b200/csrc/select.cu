@@ -1,26 +1,17 @@
 // select.cu -- a1..a3 of Algorithm 1: label-score GEMV and exact
-// top-k selection, as two kernels.
-//
-// score_kernel  (grid: chunks x units, no inter-CTA communication)
+// top-k selection, fused in one kernel (score_select_kernel, grid chunks x
+// units, 512 threads; see the kernel's comment for the three phases).
 //   a1  q_lab[j] = sum_g q[b][hG+g][C[h][j]]      (fp32, g order; reading R3)
 //   a2  s_hat[t] = fma-chain_j(q_lab[j], L[t][j])  (fp32, j ascending, no
 //       1/sqrt(d); reading R2), streamed from the contiguous label cache with
 //       eight 128-bit loads in flight per thread (one row = r*e = 16 B at
-//       r=8 / 16-bit).  Each score becomes a monotone u32 order key (-0 == +0)
-//       written to a workspace that stays in L2, plus a per-CTA histogram of
-//       the key's top 11 bits (sign, exponent, 2 mantissa bits).
-//
-// select_kernel (grid: units, one 1024-thread CTA each; __syncthreads only)
-//   a3  i = argtopk(s_hat, k): ties to the lower index, ascending (reading R6).
-//       The unit's <= 8 partial histograms are summed -> boundary digit b1;
-//       one pass over the L2-resident keys marks digit > b1 in a selection
-//       bitmap and collects the boundary digit's (key, token) candidates;
-//       these are resolved exactly by a second 11-bit level and an exact rank
-//       of the few keys left in the second boundary digit.  A tie-heavy
-//       boundary (more candidates than fit) takes an exact MSB radix select.
-//       The bitmap is compacted in token order into the index list, and each
-//       selected token's pool row id (block_table lookup) is written beside
-//       it, so the attention kernel's gathers start after a single load.
+//       r=8 / 16-bit) into a monotone u32 order key (-0 == +0) in smem.
+//   a3  i = argtopk(s_hat, k): exact, ties to the lower index, ascending
+//       (reading R6).  Each chunk emits a candidate superset of its share of
+//       the global top-k; the unit's last-arriving CTA selects exactly among
+//       them (MSB radix 12+12+8 bits, equal keys by token order) and writes
+//       the index list with each token's pool row id.  s_hat never leaves the
+//       chip; the candidates (~k + a histogram bin per chunk) stay in L2.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -30,19 +21,81 @@
 namespace ds {
 
 constexpr int kScoreThreads = 512;
+constexpr int kScoreWarps = kScoreThreads / 32;
 constexpr int kScoreUnroll = 8;
-constexpr int kMaxChunks = 8;  // score CTAs per unit (partial histograms)
+constexpr int kMaxChunks = 16;       // score CTAs per unit
+constexpr int kMaxChunkLen = 16384;  // tokens per score CTA (keys kept in smem)
+constexpr int kMaxDynSmem = 200 * 1024;
 constexpr int kMaxR = 256;
-constexpr int kDigitBits = 12;             // radix digit width
-constexpr int kBins = 1 << kDigitBits;      // digits per level
-constexpr int kShift1 = 32 - kDigitBits;    // level 1: top 12 key bits
-constexpr int kShift2 = kShift1 - kDigitBits;  // level 2: the next 12
-constexpr int kSelThreads = 1024;
-constexpr int kSelWarps = kSelThreads / 32;
-constexpr int kCandCap = 4096;
+constexpr int kDigitBits = 12;
+constexpr int kBins = 1 << kDigitBits;
+constexpr int kShift1 = 32 - kDigitBits;  // level-1 digit: top 12 key bits
 
-// per-unit stride of the key workspace: a multiple of 4 keys (16 B)
-__host__ __device__ __forceinline__ size_t key_stride(int smax) { return ((size_t)smax + 3) & ~(size_t)3; }
+// per-unit stride of the candidate workspace (>= nchunks * chunk for any geometry)
+__host__ __device__ __forceinline__ size_t cand_stride(int smax) {
+  return (size_t)smax + (size_t)kMaxChunks * 256;
+}
+
+// ------------------------------------------------------------ helpers
+// Block-wide exclusive prefix of one u32 per thread (NT threads); *total =
+// sum.  Two shuffle levels (warp, then warp 0 over the warp totals): 2
+// barriers, no serial smem walks.  warp_tot needs NT/32 + 1 entries.
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *warp_tot, uint32_t *total) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();  // warp_tot may still be read by a previous scan
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t t = lane < NW ? warp_tot[lane] : 0u;
+    uint32_t y = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += z;
+    }
+    if (lane < NW) warp_tot[lane] = y - t;
+    if (lane == NW - 1) warp_tot[NW] = y;
+  }
+  __syncthreads();
+  *total = warp_tot[NW];
+  return warp_tot[warp] + x - v;
+}
+
+// Boundary digit of a histogram bins[nb] (nb a multiple of NT): with `need`
+// keys wanted from the top, the digit d with above(d) < need <= above(d) +
+// bins[d]; every thread gets (d, above(d), bins[d]).
+template <int NT>
+__device__ __forceinline__ void find_boundary(const uint32_t *bins, int nb, uint32_t need, uint32_t *warp_tot,
+                                              uint32_t *state, uint32_t &d, uint32_t &above, uint32_t &cnt) {
+  const int per = nb / NT;  // thread t owns digits nb-1-per*t-j, descending
+  uint32_t s = 0;
+  for (int j = 0; j < per; ++j) s += bins[nb - 1 - per * (int)threadIdx.x - j];
+  uint32_t tot;
+  uint32_t run = block_excl_scan<NT>(s, warp_tot, &tot);
+  for (int j = 0; j < per; ++j) {
+    const int dd = nb - 1 - per * (int)threadIdx.x - j;
+    const uint32_t v = bins[dd];
+    if (run < need && run + v >= need) {
+      state[0] = dd;
+      state[1] = run;
+      state[2] = v;
+    }
+    run += v;
+  }
+  __syncthreads();
+  d = state[0];
+  above = state[1];
+  cnt = state[2];
+  __syncthreads();
+}
 
 // ------------------------------------------------------------------ A
 template <typename T, int R>
@@ -62,22 +115,429 @@ __device__ __forceinline__ float label_score(const T *__restrict__ row, const fl
   return s;
 }
 
+// Candidate sources for the unit's exact selection: staged in shared memory
+// (the usual case) or read in place from the per-chunk segments in global
+// memory (tie-heavy boundaries with more candidates than fit).
+struct StagedSrc {
+  const uint2 *a;
+  __device__ __forceinline__ uint2 get(int s) const { return a[s]; }
+};
+struct GlobalSrc {
+  const uint2 *g;
+  const uint32_t *seg;
+  int chunk;
+  __device__ __forceinline__ uint2 get(int s) const {
+    int q = 0;
+    while ((int)seg[q + 1] <= s) ++q;
+    return __ldcg(g + (size_t)q * chunk + (s - (int)seg[q]));
+  }
+};
+
+struct SelScratch {
+  uint32_t *bins;      // [kBins]
+  uint32_t *warp_tot;  // [NW + 1]
+  uint32_t *state;     // [4]
+};
+
+// Exact top-k_eff of T candidates (ascending token order) with ties to the
+// lower index: MSB radix over 12 + 12 + 8 key bits for the k-th key, then
+// one ordered pass writes the selected tokens (ascending) and their pool row
+// ids.  NT threads.
+template <int NT, class Src>
+__device__ __forceinline__ void select_core(const Src &src, int T, uint32_t keff, const SelScratch &sc,
+                                            int32_t *idx_out, int32_t *rid_out, const CacheView &c, int b,
+                                            int h) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t need = keff, prefix = 0, mask = 0;
+  bool whole = false;  // the boundary bin is taken entirely
+  for (int lv = 0; lv < 3 && !whole; ++lv) {
+    const int sh = lv == 0 ? 20 : (lv == 1 ? 8 : 0), nb = lv < 2 ? 4096 : 256;
+    const uint32_t wm = (uint32_t)nb - 1u;
+    const int nbz = nb < NT ? NT : nb;
+    for (int i = tid; i < nbz; i += NT) sc.bins[i] = 0;
+    __syncthreads();
+#pragma unroll 4
+    for (int s = tid; s < T; s += NT) {
+      const uint32_t key = src.get(s).x;
+      if ((key & mask) == prefix) atomicAdd(&sc.bins[(key >> sh) & wm], 1u);
+    }
+    __syncthreads();
+    uint32_t d, above, cnt;
+    find_boundary<NT>(sc.bins, nbz, need, sc.warp_tot, sc.state, d, above, cnt);
+    need -= above;
+    prefix |= d << sh;
+    mask |= wm << sh;
+    whole = cnt == need;
+  }
+  // ordered selection: masked key > prefix, or == prefix and (the whole bin
+  // is taken, or it is among the first `need` equal keys in token order)
+  int per = (T + NW - 1) / NW;
+  per = (per + 31) & ~31;
+  const int w0 = min(warp * per, T), w1 = min(w0 + per, T);
+  const uint32_t lt = lanemask_lt();
+  uint32_t tot, eq_base = 0;
+  if (!whole) {
+    uint32_t weq = 0;
+#pragma unroll 4
+    for (int base = w0; base < w1; base += 32) {
+      const int s = base + lane;
+      weq += __popc(__ballot_sync(0xffffffffu, s < w1 && (src.get(s).x & mask) == prefix));
+    }
+    eq_base = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? weq : 0u, sc.warp_tot, &tot), 0);
+  }
+  uint32_t wtake = 0, run = eq_base;
+#pragma unroll 4
+  for (int base = w0; base < w1; base += 32) {
+    const int s = base + lane;
+    const uint32_t km = s < w1 ? (src.get(s).x & mask) : 0u;
+    const bool gt = s < w1 && km > prefix, eq = s < w1 && km == prefix;
+    const uint32_t em = __ballot_sync(0xffffffffu, eq);
+    const bool take = gt || (eq && (whole || run + __popc(em & lt) < need));
+    wtake += __popc(__ballot_sync(0xffffffffu, take));
+    run += __popc(em);
+  }
+  uint32_t pos = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? wtake : 0u, sc.warp_tot, &tot), 0);
+  run = eq_base;
+  const int32_t *bt = c.block_table + (size_t)b * c.maxp;
+  const bool pow2 = (c.P & (c.P - 1)) == 0;
+  const int psh = __ffs(c.P) - 1;
+#pragma unroll 2
+  for (int base = w0; base < w1; base += 32) {
+    const int s = base + lane;
+    uint2 e = make_uint2(0u, 0u);
+    if (s < w1) e = src.get(s);
+    const uint32_t km = e.x & mask;
+    const bool gt = s < w1 && km > prefix, eq = s < w1 && km == prefix;
+    const uint32_t em = __ballot_sync(0xffffffffu, eq);
+    const bool take = gt || (eq && (whole || run + __popc(em & lt) < need));
+    const uint32_t tm = __ballot_sync(0xffffffffu, take);
+    if (take) {
+      const uint32_t o = pos + __popc(tm & lt);
+      const int t = (int)e.y;
+      const int pg = pow2 ? (t >> psh) : t / c.P;
+      const int sl = pow2 ? (t & (c.P - 1)) : t - pg * c.P;
+      idx_out[o] = t;
+      rid_out[o] = (int32_t)(((uint32_t)__ldg(bt + pg) * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P + (uint32_t)sl);
+    }
+    pos += __popc(tm);
+    run += __popc(em);
+  }
+}
+
+// select_core for candidates staged in shared memory (16-B aligned, padded
+// by 4 entries): warp w owns 128-candidate blocks; lane l handles candidates
+// 4l..4l+3 of a block (two 128-bit loads), prefix sums by warp shuffles.
+template <int NT>
+__device__ __forceinline__ void select_core_staged(const uint2 *cand, int T, uint32_t keff, const SelScratch &sc,
+                                                   int32_t *idx_out, int32_t *rid_out, const CacheView &c, int b,
+                                                   int h) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int per = (T + NW - 1) / NW;
+  per = (per + 127) & ~127;
+  const int w0 = min(warp * per, T), w1 = min(w0 + per, T);
+  auto load4 = [&](int base, uint32_t (&k)[4], uint32_t (&t)[4]) {
+    const uint4 a = *reinterpret_cast<const uint4 *>(cand + base + 4 * lane);
+    const uint4 bq = *reinterpret_cast<const uint4 *>(cand + base + 4 * lane + 2);
+    k[0] = a.x; t[0] = a.y; k[1] = a.z; t[1] = a.w;
+    k[2] = bq.x; t[2] = bq.y; k[3] = bq.z; t[3] = bq.w;
+  };
+  auto warp_excl = [&](uint32_t v, uint32_t &total) {
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
+  };
+  uint32_t need = keff, prefix = 0, mask = 0;
+  bool whole = false;
+  for (int lv = 0; lv < 3 && !whole; ++lv) {
+    const int sh = lv == 0 ? 20 : (lv == 1 ? 8 : 0), nb = lv < 2 ? 4096 : 256;
+    const uint32_t wm = (uint32_t)nb - 1u;
+    const int nbz = nb < NT ? NT : nb;
+    for (int i = tid; i < nbz; i += NT) sc.bins[i] = 0;
+    __syncthreads();
+    for (int base = w0; base < w1; base += 128) {
+      uint32_t k[4], t[4];
+      load4(base, k, t);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (base + 4 * lane + e < w1 && (k[e] & mask) == prefix) atomicAdd(&sc.bins[(k[e] >> sh) & wm], 1u);
+    }
+    __syncthreads();
+    uint32_t d, above, cnt;
+    find_boundary<NT>(sc.bins, nbz, need, sc.warp_tot, sc.state, d, above, cnt);
+    need -= above;
+    prefix |= d << sh;
+    mask |= wm << sh;
+    whole = cnt == need;
+  }
+  uint32_t tot, eq_base = 0;
+  if (!whole) {  // equal keys beyond the first `need` are dropped: their ordinals
+    uint32_t weq = 0;
+    for (int base = w0; base < w1; base += 128) {
+      uint32_t k[4], t[4];
+      load4(base, k, t);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) weq += base + 4 * lane + e < w1 && (k[e] & mask) == prefix;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) weq += __shfl_xor_sync(0xffffffffu, weq, o);
+    eq_base = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? weq : 0u, sc.warp_tot, &tot), 0);
+  }
+  // per lane: take flags for its 4 candidates (gt, or eq within the first `need`)
+  auto takes = [&](int base, const uint32_t (&k)[4], uint32_t &run, bool (&tk)[4]) {
+    bool eq[4];
+    uint32_t ne = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const bool in = base + 4 * lane + e < w1;
+      const uint32_t km = k[e] & mask;
+      eq[e] = in && km == prefix;
+      tk[e] = in && km > prefix;
+      ne += eq[e];
+    }
+    uint32_t etot;
+    uint32_t eo = run + (whole ? 0u : warp_excl(ne, etot));
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      tk[e] = tk[e] || (eq[e] && (whole || eo < need));
+      eo += eq[e];
+    }
+    if (!whole) run += etot;
+  };
+  uint32_t wtake = 0, run = eq_base;
+  for (int base = w0; base < w1; base += 128) {
+    uint32_t k[4], t[4];
+    bool tk[4];
+    load4(base, k, t);
+    takes(base, k, run, tk);
+    wtake += tk[0] + tk[1] + tk[2] + tk[3];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wtake += __shfl_xor_sync(0xffffffffu, wtake, o);
+  uint32_t pos = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? wtake : 0u, sc.warp_tot, &tot), 0);
+  run = eq_base;
+  const int32_t *bt = c.block_table + (size_t)b * c.maxp;
+  const bool pow2 = (c.P & (c.P - 1)) == 0;
+  const int psh = __ffs(c.P) - 1;
+  for (int base = w0; base < w1; base += 128) {
+    uint32_t k[4], t[4];
+    bool tk[4];
+    load4(base, k, t);
+    takes(base, k, run, tk);
+    const uint32_t nt = tk[0] + tk[1] + tk[2] + tk[3];
+    uint32_t ttot;
+    uint32_t o = pos + warp_excl(nt, ttot);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (tk[e]) {
+        const int tok = (int)t[e];
+        const int pg = pow2 ? (tok >> psh) : tok / c.P;
+        const int sl = pow2 ? (tok & (c.P - 1)) : tok - pg * c.P;
+        idx_out[o] = tok;
+        rid_out[o] = (int32_t)(((uint32_t)__ldg(bt + pg) * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P +
+                               (uint32_t)sl);
+        ++o;
+      }
+    pos += ttot;
+  }
+}
+
+// Exact top-k of T staged candidates (ascending token order), fast path:
+// level 1 = 4096 linear fp32 bins over [lo, hi] (the candidates' key range),
+// so the boundary bin holds only a few keys; the boundary is found by one warp
+// over a 64-bin coarse then a 64-bin fine scan; the boundary bin's members are
+// ranked exactly by (key desc, token asc) by one warp; one ordered pass writes
+// the selected tokens and their pool row ids.  Returns false (nothing
+// written) when the boundary bin is too crowded (ties): the caller then runs
+// the generic radix path.
+constexpr int kMaxMembers = 256;
+struct FastScratch {
+  uint32_t *fine;      // [4096]
+  uint32_t *coarse;    // [64]
+  uint2 *members;      // [kMaxMembers] (key, slot)
+  uint32_t *selbits;   // [T/32 + 1] selected boundary members, by slot
+  uint32_t *warp_tot;  // [NW + 1]
+  uint32_t *state;     // [8]
+};
+
+template <int NT>
+__device__ __forceinline__ bool select_fast(const uint2 *cand, int T, uint32_t keff, uint32_t lo_key,
+                                            uint32_t hi_key, const FastScratch &sc, int32_t *idx_out,
+                                            int32_t *rid_out, const int32_t *btrow, const CacheView &c, int h) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float lo = key_to_float(lo_key), hi = key_to_float(hi_key);
+  const float scale = 4096.0f / (hi - lo);
+  auto binof = [&](uint32_t key) -> int {
+    const float x = fminf(fmaxf((key_to_float(key) - lo) * scale, 0.0f), 4095.0f);
+    return (int)x;
+  };
+  for (int i = tid; i < 4096; i += NT) sc.fine[i] = 0;
+  if (tid < 64) sc.coarse[tid] = 0;
+  for (int i = tid; i <= T / 32; i += NT) sc.selbits[i] = 0;
+  if (tid == 0) sc.state[4] = 0;
+  __syncthreads();
+#pragma unroll 4
+  for (int s = tid; s < T; s += NT) {
+    const int bn = binof(cand[s].x);
+    atomicAdd(&sc.fine[bn], 1u);
+    atomicAdd(&sc.coarse[bn >> 6], 1u);
+  }
+  __syncthreads();
+  if (warp == 0) {  // coarse then fine boundary, descending bins
+    uint32_t above = 0;
+    int cb = 0;
+    {
+      const uint32_t a = sc.coarse[63 - 2 * lane], bq = sc.coarse[62 - 2 * lane];
+      uint32_t incl = a + bq;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t ex = incl - a - bq;
+      const bool h0 = ex < keff && ex + a >= keff;
+      const bool h1 = !h0 && ex + a < keff && ex + a + bq >= keff;
+      const uint32_t m = __ballot_sync(0xffffffffu, h0 || h1);
+      const int src = __ffs(m) - 1;
+      const bool sh1 = __shfl_sync(0xffffffffu, h1, src);
+      cb = 63 - 2 * src - (sh1 ? 1 : 0);
+      above = __shfl_sync(0xffffffffu, sh1 ? ex + a : ex, src);
+    }
+    {
+      const int f0 = cb * 64;
+      const uint32_t a = sc.fine[f0 + 63 - 2 * lane], bq = sc.fine[f0 + 62 - 2 * lane];
+      uint32_t incl = a + bq;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t ex = above + incl - a - bq;
+      const bool h0 = ex < keff && ex + a >= keff;
+      const bool h1 = !h0 && ex + a < keff && ex + a + bq >= keff;
+      const uint32_t m = __ballot_sync(0xffffffffu, h0 || h1);
+      const int src = __ffs(m) - 1;
+      if (lane == src) {
+        sc.state[0] = f0 + 63 - 2 * lane - (h1 ? 1 : 0);
+        sc.state[1] = h1 ? ex + a : ex;
+        sc.state[2] = h1 ? bq : a;
+      }
+    }
+  }
+  __syncthreads();
+  const int b1 = (int)sc.state[0];
+  const uint32_t need = keff - sc.state[1], cnt = sc.state[2];
+  const bool whole = cnt == need;
+  if (!whole) {
+    if (cnt > (uint32_t)kMaxMembers) return false;
+    // members of the boundary bin -> list, ranked exactly by warp 0
+#pragma unroll 4
+    for (int s = tid; s < T; s += NT) {
+      const uint32_t key = cand[s].x;
+      if (binof(key) == b1) sc.members[atomicAdd(&sc.state[4], 1u)] = make_uint2(key, (uint32_t)s);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int m = (int)sc.state[4];
+      for (int i = lane; i < m; i += 32) {
+        const uint2 me = sc.members[i];
+        uint32_t rank = 0;
+        for (int j = 0; j < m; ++j) {
+          const uint2 o = sc.members[j];
+          rank += (o.x > me.x) || (o.x == me.x && o.y < me.y);  // slot order == token order
+        }
+        if (rank < need) atomicOr(&sc.selbits[me.y >> 5], 1u << (me.y & 31));
+      }
+    }
+    __syncthreads();
+  }
+  // ---- ordered pass: warp w owns a contiguous slot range
+  int per = (T + NW - 1) / NW;
+  per = (per + 31) & ~31;
+  const int w0 = min(warp * per, T), w1 = min(w0 + per, T);
+  auto take = [&](int s, uint32_t key) {
+    const int bn = binof(key);
+    return bn > b1 || (bn == b1 && (whole || ((sc.selbits[s >> 5] >> (s & 31)) & 1u)));
+  };
+  uint32_t wt = 0;
+#pragma unroll 4
+  for (int base = w0; base < w1; base += 32) {
+    const int s = base + lane;
+    wt += __popc(__ballot_sync(0xffffffffu, s < w1 && take(s, cand[s].x)));
+  }
+  uint32_t tot;
+  uint32_t pos = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? wt : 0u, sc.warp_tot, &tot), 0);
+  const uint32_t lt = lanemask_lt();
+  const bool pow2 = (c.P & (c.P - 1)) == 0;
+  const int psh = __ffs(c.P) - 1;
+#pragma unroll 2
+  for (int base = w0; base < w1; base += 32) {
+    const int s = base + lane;
+    uint2 e = make_uint2(0u, 0u);
+    if (s < w1) e = cand[s];
+    const bool tk = s < w1 && take(s, e.x);
+    const uint32_t tm = __ballot_sync(0xffffffffu, tk);
+    if (tk) {
+      const uint32_t o = pos + __popc(tm & lt);
+      const int t = (int)e.y;
+      const int pg = pow2 ? (t >> psh) : t / c.P;
+      const int sl = pow2 ? (t & (c.P - 1)) : t - pg * c.P;
+      idx_out[o] = t;
+      rid_out[o] = (int32_t)(((uint32_t)btrow[pg] * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P + (uint32_t)sl);
+    }
+    pos += __popc(tm);
+  }
+  return true;
+}
+
+// Fused a1 + a2 + a3.  Grid (chunks, units), kScoreThreads threads.
+//   1. stream this chunk's label rows -> keys (smem) + 12-bit digit histogram
+//   2. emit, in token order, every token whose digit is >= the digit bounding
+//      the chunk's local top-k: a superset of the chunk's share of the unit's
+//      global top-k (any global top-k token is in its chunk's top-k)
+//   3. the last CTA of the unit to arrive (global counter) selects exactly
+//      among the unit's candidates, writes the index list and row ids, resets
+//      the counter and publishes ready[unit] for the attention kernel
+// counter[] and ready[] are zero between calls (zero-filled workspace on first
+// use; restored by the last arriver and by the attention kernel).
 template <typename T, int R>
-__global__ void __launch_bounds__(kScoreThreads) score_kernel(ScoreParams p) {
+__global__ void __launch_bounds__(kScoreThreads, 2) score_select_kernel(ScoreParams p) {
+  extern __shared__ __align__(16) uint32_t keys[];  // [chunk] order keys; then staged candidates
+  __shared__ float qlab[kMaxR];
+  __shared__ __align__(16) uint32_t hist[kBins];
+  __shared__ uint32_t warp_tot[kScoreWarps + 1], state[8], seg[kMaxChunks + 1];
+  __shared__ uint32_t coarse[64], mm[2];
+  __shared__ __align__(16) uint2 members[kMaxMembers];
+  __shared__ int last;
   const CacheView &c = p.c;
   const int unit = blockIdx.y, part = blockIdx.x;
   const int b = unit / c.Hkv, h = unit - (unit / c.Hkv) * c.Hkv;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = c.seq_lens[b];
   const int t0 = part * p.chunk;
   const int nloc = min(p.chunk, n - t0);
   const int r = R > 0 ? R : c.r;
+  const int keff = min(p.k, n);
+  const int nparts = (n + p.chunk - 1) / p.chunk;
   DS_TRACE_AT(0, 0);
-  __shared__ float qlab[kMaxR];
-  __shared__ __align__(16) uint32_t hist[kBins];
   for (int i = tid; i < kBins; i += kScoreThreads) hist[i] = 0;
   pdl_wait();  // the label rows may come from the preceding append
   pdl_trigger();
+  if (n <= 0) {  // empty sequence: nothing selected (the attention writes zeros)
+    if (part == 0 && !p.scores)
+      for (int i = tid; i < p.k; i += kScoreThreads) {
+        p.idx[(size_t)unit * p.k + i] = -1;
+        p.rowid[(size_t)unit * p.k + i] = -1;
+      }
+    return;
+  }
   if (nloc <= 0) return;
   for (int j = tid; j < r; j += kScoreThreads) {  // a1
     const T *qb = (const T *)p.q + ((size_t)b * c.Hq + (size_t)h * c.G) * c.D;
@@ -94,13 +554,13 @@ __global__ void __launch_bounds__(kScoreThreads) score_kernel(ScoreParams p) {
   }
   const float *qs = R > 0 ? ql : qlab;
   const T *lab = (const T *)c.label + (((size_t)b * c.Hkv + h) * c.Smax + t0) * (size_t)c.r;
-  const size_t obase = (size_t)unit * c.Smax + t0;
 
   if (p.scores) {  // diagnostics entry (ds_approx_scores): s_hat to HBM
-    for (int i = tid; i < nloc; i += kScoreThreads) p.scores[obase + i] = label_score<T, R>(lab + (size_t)i * r, qs, r);
+    float *so = p.scores + (size_t)unit * c.Smax + t0;
+    for (int i = tid; i < nloc; i += kScoreThreads) so[i] = label_score<T, R>(lab + (size_t)i * r, qs, r);
     return;
   }
-  uint32_t *keys = p.keys + (size_t)unit * key_stride(c.Smax) + t0;
+  // ---- a2: stream the label: keys + digit histogram
   int i0 = tid;
   if constexpr (R > 0 && R * sizeof(T) == 16) {
     constexpr int U = kScoreUnroll;
@@ -127,396 +587,235 @@ __global__ void __launch_bounds__(kScoreThreads) score_kernel(ScoreParams p) {
     atomicAdd(&hist[k0 >> kShift1], 1u);
   }
   __syncthreads();
-  uint4 *dst = reinterpret_cast<uint4 *>(p.part_hist + ((size_t)unit * kMaxChunks + part) * kBins);
-  for (int i = tid; i < kBins / 4; i += kScoreThreads) dst[i] = reinterpret_cast<const uint4 *>(hist)[i];
   DS_TRACE_AT(0, 1);
-}
 
-// ------------------------------------------------------------------ B
-struct SelSmem {
-  uint32_t bins[kBins];
-  uint32_t warp_tot[kSelWarps];
-  uint32_t state[4];
-  uint32_t ncand, nfinal;
-  uint2 cand[kCandCap];  // (key, token)
-};
-
-// Block-wide exclusive prefix of one u32 per thread; *total gets the sum.
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *warp_tot, uint32_t *total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+  // ---- local candidates (ordered emission; warp w owns a contiguous range)
+  uint32_t dmin = 0;
+  if (keff < nloc) {
+    uint32_t above, cnt;
+    find_boundary<kScoreThreads>(hist, kBins, (uint32_t)keff, warp_tot, state, dmin, above, cnt);
   }
-  __syncthreads();
-  if (lane == 31) warp_tot[warp] = x;
-  __syncthreads();
-  uint32_t before = 0, tot = 0;
-  for (int w = 0; w < kSelWarps; ++w) {
-    const uint32_t t = warp_tot[w];
-    before += w < warp ? t : 0u;
-    tot += t;
-  }
-  *total = tot;
-  return before + x - v;
-}
-
-// Boundary digit of the histogram in sm.bins: with `need` keys wanted from the
-// top, the digit d with above(d) < need <= above(d) + bins[d]; all threads get
-// (d, above(d), bins[d]).
-__device__ __forceinline__ void find_boundary(SelSmem &sm, uint32_t need, uint32_t &d, uint32_t &above,
-                                              uint32_t &cnt) {
-  constexpr int PER = kBins / kSelThreads;
-  const int tid = threadIdx.x;
-  uint32_t v[PER], s = 0;  // thread tid owns digits kBins-1-PER*tid-j (descending order)
-#pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    v[j] = sm.bins[kBins - 1 - PER * tid - j];
-    s += v[j];
-  }
-  uint32_t tot;
-  uint32_t run = block_excl_scan(s, sm.warp_tot, &tot);
-#pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    if (run < need && run + v[j] >= need) {
-      sm.state[0] = kBins - 1 - PER * tid - j;
-      sm.state[1] = run;
-      sm.state[2] = v[j];
+  {
+    // warp w owns 128-token blocks [w0, w1); lane l holds tokens 4l..4l+3 of
+    // a block (one 128-bit smem load); positions by warp-shuffle prefix sums
+    int per = (nloc + kScoreWarps - 1) / kScoreWarps;
+    per = (per + 127) & ~127;
+    const int w0 = min(warp * per, nloc), w1 = min(w0 + per, nloc);
+    uint32_t mine = 0, kmin = 0xffffffffu, kmax = 0u;
+    if (tid == 0) {
+      mm[0] = 0xffffffffu;
+      mm[1] = 0u;
     }
-    run += v[j];
-  }
-  __syncthreads();
-  d = sm.state[0];
-  above = sm.state[1];
-  cnt = sm.state[2];
-  __syncthreads();
-}
-
-// Ordered compaction of the selection bitmap: token t -> position
-// #selected(< t), with its pool row id.
-__device__ __forceinline__ void compact(SelSmem &sm, const uint32_t *bm, int nwords, int32_t *idx_out,
-                                        int32_t *rowid_out, const CacheView &c, const int32_t *bt, int h) {
-  const int tid = threadIdx.x;
-  const int per = (nwords + kSelThreads - 1) / kSelThreads;
-  const int w0 = min(tid * per, nwords), w1 = min(w0 + per, nwords);
-  uint32_t cnt = 0;
-  for (int w = w0; w < w1; ++w) cnt += __popc(bm[w]);
-  uint32_t tot;
-  uint32_t pos = block_excl_scan(cnt, sm.warp_tot, &tot);
-  for (int w = w0; w < w1; ++w) {
-    uint32_t bits = bm[w];
-    while (bits) {  // up to 4 tokens at a time
-      int tt[4];
+#pragma unroll 2
+    for (int base = w0; base < w1; base += 128) {
+      const int i = base + 4 * lane;
+      const uint4 kv = *reinterpret_cast<const uint4 *>(keys + i);
+      const uint32_t kk[4] = {kv.x, kv.y, kv.z, kv.w};
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        tt[u] = bits ? w * 32 + __ffs(bits) - 1 : -1;
-        bits &= bits - 1;
+      for (int e = 0; e < 4; ++e)
+        if (i + e < w1 && (kk[e] >> kShift1) >= dmin) {
+          ++mine;
+          kmin = min(kmin, kk[e]);
+          kmax = max(kmax, kk[e]);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mine += __shfl_xor_sync(0xffffffffu, mine, o);
+      kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+      kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (lane == 0) {
+      atomicMin(&mm[0], kmin);
+      atomicMax(&mm[1], kmax);
+    }
+    uint32_t tot;
+    uint32_t pos = __shfl_sync(0xffffffffu, block_excl_scan<kScoreThreads>(lane == 0 ? mine : 0u, warp_tot, &tot), 0);
+    uint2 *out = p.cand + (size_t)unit * cand_stride(c.Smax) + (size_t)part * p.chunk;
+#pragma unroll 2
+    for (int base = w0; base < w1; base += 128) {
+      const int i = base + 4 * lane;
+      const uint4 kv = *reinterpret_cast<const uint4 *>(keys + i);
+      const uint32_t kk[4] = {kv.x, kv.y, kv.z, kv.w};
+      bool sel[4];
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        sel[e] = i + e < w1 && (kk[e] >> kShift1) >= dmin;
+        cnt += sel[e];
       }
-      int pg[4];
+      uint32_t incl = cnt;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) pg[u] = tt[u] >= 0 ? bt[tt[u] / c.P] : 0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (tt[u] < 0) break;
-        idx_out[pos] = tt[u];
-        rowid_out[pos] = (int32_t)(((uint32_t)pg[u] * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P +
-                                   (uint32_t)(tt[u] % c.P));
-        ++pos;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
       }
+      uint32_t o = pos + incl - cnt;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (sel[e]) out[o++] = make_uint2(kk[e], (uint32_t)(t0 + i + e));
+      pos += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      p.cand_count[unit * kMaxChunks + part] = tot;
+      p.cand_minmax[(unit * kMaxChunks + part) * 2] = mm[0];
+      p.cand_minmax[(unit * kMaxChunks + part) * 2 + 1] = mm[1];
     }
   }
-}
+  DS_TRACE_AT(0, 2);
 
-// Spread the 8 bits of x to bit positions 0, 4, ..., 28.
-__device__ __forceinline__ uint32_t spread4(uint32_t x) {
-  x = (x | (x << 12)) & 0x000F000Fu;
-  x = (x | (x << 6)) & 0x03030303u;
-  x = (x | (x << 3)) & 0x11111111u;
-  return x;
-}
-
-__global__ void __launch_bounds__(kSelThreads) select_kernel(SelectParams p) {
-  extern __shared__ __align__(16) uint8_t dyn[];
-  SelSmem &sm = *reinterpret_cast<SelSmem *>(dyn);
-  uint32_t *bm = reinterpret_cast<uint32_t *>(dyn + sizeof(SelSmem));  // [Smax/32] selection bitmap
-  int32_t *btrow = reinterpret_cast<int32_t *>(bm + ((p.c.Smax + 31) >> 5));  // [maxp] this sequence's pages
-  const CacheView &c = p.c;
-  const int unit = blockIdx.x;
-  const int b = unit / c.Hkv, h = unit - (unit / c.Hkv) * c.Hkv;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int n = c.seq_lens[b];
-  const int keff = min(p.k, n);
-  const int nwords = (n + 31) >> 5;
+  // ---- arrival: the unit's last CTA performs the selection
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();  // release this CTA's candidates
+    last = atomicAdd(p.counter + unit, 1u) == (uint32_t)(nparts - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();  // acquire the other chunks' candidates
+  if (tid == 0) {
+    uint32_t o = 0, lo = 0xffffffffu, hi = 0u;
+    for (int q = 0; q < nparts; ++q) {
+      seg[q] = o;
+      o += __ldcg(p.cand_count + unit * kMaxChunks + q);
+      lo = min(lo, __ldcg(p.cand_minmax + (unit * kMaxChunks + q) * 2));
+      hi = max(hi, __ldcg(p.cand_minmax + (unit * kMaxChunks + q) * 2 + 1));
+    }
+    seg[nparts] = o;
+    mm[0] = lo;
+    mm[1] = hi;
+  }
+  __syncthreads();
+  const int ncand = (int)seg[nparts];
+  const uint2 *gc = p.cand + (size_t)unit * cand_stride(c.Smax);
   int32_t *idx_out = p.idx + (size_t)unit * p.k;
   int32_t *rid_out = p.rowid + (size_t)unit * p.k;
-  const uint32_t *keys = p.keys + (size_t)unit * key_stride(c.Smax);
-  DS_TRACE_AT(1, 0);
-
-  {
-    const int np = (n + c.P - 1) / c.P;
-    const int32_t *bt = c.block_table + (size_t)b * c.maxp;
-    for (int i = tid; i < np; i += kSelThreads) btrow[i] = __ldg(bt + i);
-  }
-  for (int i = keff + tid; i < p.k; i += kSelThreads) {  // positions >= k_eff
+  for (int i = keff + tid; i < p.k; i += kScoreThreads) {  // positions >= k_eff
     idx_out[i] = -1;
     rid_out[i] = -1;
   }
-  if (tid == 0) {
-    sm.ncand = 0;
-    sm.nfinal = 0;
-  }
-  pdl_wait();  // keys and partial histograms come from score_kernel
-  pdl_trigger();
-  if (keff >= n) {  // every token selected (k >= S, or a short sequence)
-    for (int w = tid; w < nwords; w += kSelThreads)
-      bm[w] = (w == nwords - 1 && (n & 31)) ? (1u << (n & 31)) - 1u : 0xffffffffu;
-    __syncthreads();
-    compact(sm, bm, nwords, idx_out, rid_out, c, btrow, h);
-    return;
-  }
-
-  // ---- level 1: sum the partial histograms of the score CTAs
-  const int nparts = (n + p.chunk - 1) / p.chunk;
-  for (int i = tid; i < kBins; i += kSelThreads) {
-    uint32_t v[kMaxChunks];
+  const SelScratch scr{hist, warp_tot, state};
+  uint2 *stage = reinterpret_cast<uint2 *>(keys);  // the keys are no longer needed
+  int32_t *btrow = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(keys) + (size_t)p.stage_cap * 8);
+  uint32_t *selbits = reinterpret_cast<uint32_t *>(btrow + c.maxp);
+  bool done = false;
+  if (ncand + 128 <= p.stage_cap) {  // vector loads read up to 127 entries past the end
+    // the block-table row (row ids) and every chunk's candidates: each thread
+    // issues a batch of loads into registers before storing any of them, so
+    // the L2 round trips overlap instead of serialising on the smem stores
+    {
+      const int np = (n + c.P - 1) / c.P;
+      const int32_t *bt = c.block_table + (size_t)b * c.maxp;
+      constexpr int BU = 8;
+      for (int i0 = tid; i0 < np; i0 += BU * kScoreThreads) {
+        int32_t v[BU];
 #pragma unroll
-    for (int q = 0; q < kMaxChunks; ++q)
-      v[q] = q < nparts ? __ldcg(p.part_hist + ((size_t)unit * kMaxChunks + q) * kBins + i) : 0u;
-    uint32_t s = 0;
+        for (int u = 0; u < BU; ++u) v[u] = i0 + u * kScoreThreads < np ? __ldg(bt + i0 + u * kScoreThreads) : 0;
 #pragma unroll
-    for (int q = 0; q < kMaxChunks; ++q) s += v[q];
-    sm.bins[i] = s;
-  }
-  __syncthreads();
-  uint32_t b1, above1, cnt1;
-  find_boundary(sm, (uint32_t)keff, b1, above1, cnt1);
-  DS_TRACE_AT(1, 1);
-  const uint32_t rem1 = (uint32_t)keff - above1;
-  const bool take_all = cnt1 == rem1;
-
-  if (take_all || cnt1 <= (uint32_t)kCandCap) {
-    // ---- one pass over the keys: bitmap of digit > b1 (and == b1 when all of
-    // it is taken), boundary candidates into smem.  A warp covers 32
-    // consecutive tokens per round (one bitmap word).
-    // A warp round covers 128 consecutive tokens: lane l holds tokens
-    // base+4l .. base+4l+3 (one 128-bit load); the 4 bitmap words of the
-    // round are assembled from 4 ballots.  RB rounds of loads in flight.
-    constexpr int RB = 8, TPR = kSelThreads * 4;
-    const int rounds = (n + TPR - 1) / TPR;
-    for (int rd0 = 0; rd0 < rounds; rd0 += RB) {
-      uint4 kv[RB];
-#pragma unroll
-      for (int u = 0; u < RB; ++u) {
-        const int t = (rd0 + u) * TPR + 4 * tid;
-        kv[u] = t < n ? __ldcg(reinterpret_cast<const uint4 *>(keys + t)) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < BU; ++u)
+          if (i0 + u * kScoreThreads < np) btrow[i0 + u * kScoreThreads] = v[u];
       }
+      for (int s0 = tid; s0 < ncand; s0 += BU * kScoreThreads) {
+        uint2 v[BU];
 #pragma unroll
-      for (int u = 0; u < RB; ++u) {
-        if (rd0 + u >= rounds) break;
-        const int base = (rd0 + u) * TPR + (tid & ~31) * 4;
-        const int tl = base + 4 * lane;
-        const uint32_t kk[4] = {kv[u].x, kv[u].y, kv[u].z, kv[u].w};
-        uint32_t sb[4], cb[4];
-        int mycand = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const bool in = tl + e < n;
-          const uint32_t d = kk[e] >> kShift1;
-          sb[e] = __ballot_sync(0xffffffffu, in && (d > b1 || (take_all && d == b1)));
-          const bool cand = !take_all && in && d == b1;
-          cb[e] = __ballot_sync(0xffffffffu, cand);
-          mycand += cand;
-        }
-        if (lane < 4 && base + 32 * lane < n) {
-          uint32_t word = 0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) word |= spread4((sb[e] >> (8 * lane)) & 0xffu) << e;
-          bm[(base >> 5) + lane] = word;
-        }
-        if ((cb[0] | cb[1] | cb[2] | cb[3]) != 0u) {
-          // slots: warp-inclusive prefix of the per-lane candidate counts
-          int incl = mycand;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-          }
-          uint32_t slot = 0;
-          if (lane == 31) slot = atomicAdd(&sm.ncand, (uint32_t)incl);
-          slot = __shfl_sync(0xffffffffu, slot, 31) + (uint32_t)(incl - mycand);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint32_t d = kk[e] >> kShift1;
-            if (tl + e < n && d == b1) sm.cand[slot++] = make_uint2(kk[e], (uint32_t)(tl + e));
+        for (int u = 0; u < BU; ++u) {
+          const int s2 = s0 + u * kScoreThreads;
+          if (s2 < ncand) {
+            int q = 0;
+            while ((int)seg[q + 1] <= s2) ++q;
+            v[u] = __ldcg(gc + (size_t)q * p.chunk + (s2 - (int)seg[q]));
           }
         }
+#pragma unroll
+        for (int u = 0; u < BU; ++u)
+          if (s0 + u * kScoreThreads < ncand) stage[s0 + u * kScoreThreads] = v[u];
       }
     }
     __syncthreads();
-    DS_TRACE_AT(1, 2);
-    if (!take_all) {
-      // ---- level 2 over the candidates: the next 11 bits
-      const int nc = (int)sm.ncand;
-      for (int i = tid; i < kBins; i += kSelThreads) sm.bins[i] = 0;
-      __syncthreads();
-      for (int i = tid; i < nc; i += kSelThreads) atomicAdd(&sm.bins[(sm.cand[i].x >> kShift2) & (kBins - 1)], 1u);
-      __syncthreads();
-      uint32_t b2, above2, cnt2;
-      find_boundary(sm, rem1, b2, above2, cnt2);
-      const uint32_t rem2 = rem1 - above2;
-      uint2 *fin = sm.cand + nc;  // keys of digit b2 (when ranked) reuse the buffer tail
-      const int fcap = kCandCap - nc;
-      for (int i = tid; i < nc; i += kSelThreads) {
-        const uint2 e = sm.cand[i];
-        const uint32_t d2 = (e.x >> kShift2) & (kBins - 1);
-        if (d2 > b2 || (cnt2 == rem2 && d2 == b2)) {
-          atomicOr(&bm[e.y >> 5], 1u << (e.y & 31));
-        } else if (d2 == b2) {
-          const uint32_t s = atomicAdd(&sm.nfinal, 1u);
-          if ((int)s < fcap) fin[s] = e;
-        }
-      }
-      __syncthreads();
-      if (cnt2 != rem2) {  // exact rank (key desc, token asc) inside digit b2
-        const int nf = (int)sm.nfinal;
-        const bool small = nf <= fcap;
-        const uint2 *lst = small ? fin : sm.cand;
-        const int nl = small ? nf : nc;
-        for (int i = tid; i < nl; i += kSelThreads) {
-          const uint2 me = lst[i];
-          if (((me.x >> kShift2) & (kBins - 1)) != b2) continue;
-          uint32_t rank = 0;
-          for (int j = 0; j < nl; ++j) {
-            const uint2 o = lst[j];
-            if (((o.x >> kShift2) & (kBins - 1)) != b2) continue;
-            rank += (o.x > me.x) || (o.x == me.x && o.y < me.y);
-          }
-          if (rank < rem2) atomicOr(&bm[me.y >> 5], 1u << (me.y & 31));
-        }
-      }
-      __syncthreads();
-    }
+    DS_TRACE_AT(0, 3);
+    const FastScratch fs{hist, coarse, members, selbits, warp_tot, state};
+    done = select_fast<kScoreThreads>(stage, ncand, (uint32_t)keff, mm[0], mm[1], fs, idx_out, rid_out, btrow, c, h);
+    if (!done) select_core_staged<kScoreThreads>(stage, ncand, (uint32_t)keff, scr, idx_out, rid_out, c, b, h);
   } else {
-    // ---- exact MSB radix over the remaining 21 key bits (tie-heavy boundary)
-    uint32_t prefix = b1 << kShift1, mask = 0xffffffffu << kShift1, rem = rem1;
-    const int shs[3] = {kShift1 - 8, kShift1 - 16, 0}, nbs[3] = {8, 8, kShift1 - 16};
-    for (int ps = 0; ps < 3; ++ps) {
-      const int sh = shs[ps];
-      const uint32_t dm = (1u << nbs[ps]) - 1u;
-      for (int i = tid; i < 256; i += kSelThreads) sm.bins[i] = 0;
-      __syncthreads();
-      for (int t = tid; t < n; t += kSelThreads) {
-        const uint32_t key = __ldcg(keys + t);
-        if ((key & mask) == prefix) atomicAdd(&sm.bins[(key >> sh) & dm], 1u);
-      }
-      __syncthreads();
-      if (tid == 0) {
-        uint32_t above = 0;
-        for (int dd = (int)dm; dd >= 0; --dd) {
-          if (above + sm.bins[dd] >= rem) {
-            sm.state[0] = dd;
-            sm.state[1] = above;
-            sm.state[2] = sm.bins[dd];
-            break;
-          }
-          above += sm.bins[dd];
-        }
-      }
-      __syncthreads();
-      rem -= sm.state[1];
-      prefix |= sm.state[0] << sh;
-      mask |= dm << sh;
-      const bool done = sm.state[2] == rem;
-      __syncthreads();
-      if (done) break;
-    }
-    // gt: (key & mask) > prefix; eq: == prefix, the first `rem` by token index
-    uint32_t eq_before = 0;
-    const int rounds = (n + kSelThreads - 1) / kSelThreads;
-    for (int rd = 0; rd < rounds; ++rd) {
-      const int base = rd * kSelThreads + (tid & ~31);
-      const int t = base + lane;
-      const uint32_t km = (t < n ? __ldcg(keys + t) : 0u) & mask;
-      const bool gt = t < n && km > prefix;
-      const bool eq = t < n && km == prefix;
-      const uint32_t em = __ballot_sync(0xffffffffu, eq);
-      uint32_t tot;
-      const uint32_t wb = block_excl_scan(lane == 0 ? (uint32_t)__popc(em) : 0u, sm.warp_tot, &tot);
-      const uint32_t rk = eq_before + __shfl_sync(0xffffffffu, wb, 0) + __popc(em & lanemask_lt());
-      const uint32_t word = __ballot_sync(0xffffffffu, gt || (eq && rk < rem));
-      if (lane == 0 && base < n) bm[base >> 5] = word;
-      eq_before += tot;
-    }
-    __syncthreads();
+    select_core<kScoreThreads>(GlobalSrc{gc, seg, p.chunk}, ncand, (uint32_t)keff, scr, idx_out, rid_out, c, b, h);
   }
-  DS_TRACE_AT(1, 3);
-  compact(sm, bm, nwords, idx_out, rid_out, c, btrow, h);
-  DS_TRACE_AT(1, 4);
+  DS_TRACE_AT(0, 4);
+  // ---- publish
+  __syncthreads();
+  if (tid == 0) {
+    p.counter[unit] = 0u;
+    __threadfence();
+    atomicExch(p.ready + unit, 1u);
+  }
 }
 
 // ------------------------------------------------------------- launch
 template <typename T, int R>
-static cudaError_t launch_score_t(const ScoreParams &p, int units, int nchunks, cudaStream_t st) {
-  return PdlLaunch(dim3(nchunks, units), dim3(kScoreThreads), 0, st).run(score_kernel<T, R>, p);
+static cudaError_t launch_score_t(const ScoreParams &p, int units, int nchunks, size_t smem, cudaStream_t st) {
+  static const cudaError_t attr = cudaFuncSetAttribute(score_select_kernel<T, R>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  if (attr != cudaSuccess) return attr;
+  return PdlLaunch(dim3(nchunks, units), dim3(kScoreThreads), smem, st).run(score_select_kernel<T, R>, p);
 }
 
-SelectGeom select_geom(const ds_cache *c) {
+SelectGeom select_geom(const ds_cache *c, int k) {
   SelectGeom g{};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int units = c->batch * c->num_kv_heads;
-  // as many score CTAs per unit as fit in one wave (no straggler wave)
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel<__nv_bfloat16, 8>, kScoreThreads, 0) !=
-          cudaSuccess ||
-      per_sm < 1) {
-    cudaGetLastError();
-    per_sm = 2;
-  }
+  // CTAs per unit: enough for one wave at 2 CTAs/SM, but chunks of >= 4k
+  // tokens so that each chunk's local top-k superset stays small (~k); each
+  // chunk's keys fit in shared memory
+  const int per_sm = 2;
   int nch = (per_sm * sms) / units;
+  const int kk = k < 1 ? 1 : k;
+  const int by_k = c->max_seq_len / (4 * kk);
+  if (nch > by_k) nch = by_k;
+  const int need = (c->max_seq_len + kMaxChunkLen - 1) / kMaxChunkLen;
+  if (nch < need) nch = need;
   nch = nch < 1 ? 1 : (nch > kMaxChunks ? kMaxChunks : nch);
   int chunk = (c->max_seq_len + nch - 1) / nch;
   chunk = (chunk + 255) & ~255;
   g.chunk = chunk;
   g.nchunks = (c->max_seq_len + chunk - 1) / chunk;
-  g.smem = sizeof(SelSmem) + (size_t)((c->max_seq_len + 31) / 32) * 4 + (size_t)c->max_pages_per_seq * 4;
-  g.threads = kSelThreads;
+  // dynamic smem holds the chunk's keys, then the unit's staged candidates
+  // (expected ~nchunks * (k + a bin); the global path covers overflow)
+  size_t stage = (size_t)g.nchunks * (kk + kk / 2) + 64;
+  // the stage, the block-table row and the bitmap must fit kMaxDynSmem
+  const size_t fixed = (size_t)c->max_pages_per_seq * 4 + 4096 + 1024;
+  const size_t cap_max = (kMaxDynSmem - fixed) / (8 + 1);
+  if (stage > cap_max) stage = cap_max;
+  size_t bytes = (size_t)chunk * 4;
+  if (stage * 8 > bytes) bytes = stage * 8;
+  bytes += 1024;  // 128-bit loads run up to 127 keys / candidates past the end
+  g.stage_cap = (int)(bytes / 8);
+  // after the stage: the block-table row and the selected-members bitmap
+  bytes += (size_t)c->max_pages_per_seq * 4 + ((size_t)g.stage_cap / 32 + 1) * 4;
+  g.score_smem = (bytes + 15) & ~(size_t)15;
+  g.threads = kScoreThreads;
   return g;
 }
 
-size_t select_workspace_keys(const ds_cache *c) {
-  return (size_t)c->batch * c->num_kv_heads * key_stride(c->max_seq_len) * 4;
+size_t select_workspace_cand(const ds_cache *c) {
+  return (size_t)c->batch * c->num_kv_heads * cand_stride(c->max_seq_len) * 8;
 }
-size_t select_workspace_hist(const ds_cache *c) {
-  return (size_t)c->batch * c->num_kv_heads * kMaxChunks * kBins * 4;
-}
+size_t select_workspace_count(const ds_cache *c) { return (size_t)c->batch * c->num_kv_heads * kMaxChunks * 4; }
 
 cudaError_t launch_score(const ds_cache *c, const ScoreParams &p, const SelectGeom &g, cudaStream_t st) {
   const int units = c->batch * c->num_kv_heads;
+  if (g.chunk > kMaxChunkLen) return cudaErrorInvalidValue;
+#define DS_SCORE(T, R) launch_score_t<T, R>(p, units, g.nchunks, g.score_smem, st)
   switch (c->dtype) {
     case DS_BF16:
-      return c->r == 8 ? launch_score_t<__nv_bfloat16, 8>(p, units, g.nchunks, st)
-                       : (c->r == 16 ? launch_score_t<__nv_bfloat16, 16>(p, units, g.nchunks, st)
-                                     : launch_score_t<__nv_bfloat16, 0>(p, units, g.nchunks, st));
+      return c->r == 8 ? DS_SCORE(__nv_bfloat16, 8) : (c->r == 16 ? DS_SCORE(__nv_bfloat16, 16) : DS_SCORE(__nv_bfloat16, 0));
     case DS_FP16:
-      return c->r == 8 ? launch_score_t<__half, 8>(p, units, g.nchunks, st)
-                       : (c->r == 16 ? launch_score_t<__half, 16>(p, units, g.nchunks, st)
-                                     : launch_score_t<__half, 0>(p, units, g.nchunks, st));
+      return c->r == 8 ? DS_SCORE(__half, 8) : (c->r == 16 ? DS_SCORE(__half, 16) : DS_SCORE(__half, 0));
     default:
-      return c->r == 16 ? launch_score_t<float, 16>(p, units, g.nchunks, st)
-                        : (c->r == 8 ? launch_score_t<float, 8>(p, units, g.nchunks, st)
-                                     : launch_score_t<float, 0>(p, units, g.nchunks, st));
+      return c->r == 16 ? DS_SCORE(float, 16) : (c->r == 8 ? DS_SCORE(float, 8) : DS_SCORE(float, 0));
   }
-}
-
-cudaError_t launch_select(const ds_cache *c, const SelectParams &p, const SelectGeom &g, cudaStream_t st) {
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  if (attr != cudaSuccess) return attr;
-  return PdlLaunch(dim3(c->batch * c->num_kv_heads), dim3(kSelThreads), g.smem, st).run(select_kernel, p);
+#undef DS_SCORE
 }
 
 }  // namespace ds

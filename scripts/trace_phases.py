@@ -15,6 +15,10 @@ import synth
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 cfg = synth.CONFIGS[name]
+for kv in sys.argv[2:]:  # overrides, e.g. B=1 Hkv=1 Hq=4
+    key, val = kv.split("=")
+    cfg = cfg.with_(**{key: int(val)})
+print(cfg)
 lay = synth.make_layer(cfg, cfg.seed_base, device="cuda")
 cache = ds.LayerCache.allocate(cfg.B, cfg.Hq, cfg.Hkv, cfg.d, cfg.S, cfg.r, synth.DTYPES[cfg.dtype], lay.block_table,
                                num_pages=lay.num_pages, page_size=cfg.page_size, channel_idx=lay.C_plant)
@@ -37,21 +41,42 @@ L.ds_debug_read_trace(buf.ctypes.data_as(ctypes.c_void_p), buf.nbytes)
 
 def report(kind, names):
     t = buf[kind].astype(np.int64)
-    live = t[:, 0] > 0
-    t = t[live]
+    t = t[t[:, 0] > 0]
     if len(t) == 0:
         print("no trace for kind", kind)
         return
     t0 = min(buf[k][buf[k][:, 0] > 0][:, 0].min() for k in range(3) if (buf[k][:, 0] > 0).any())
-    print(f"\n{['score', 'select', 'attention'][kind]}: {len(t)} CTAs, span {(t[:, len(names) - 1].max() - t0) / 1e3:.2f} us")
+    print(f"\n{['score_select', 'select', 'attention'][kind]}: {len(t)} CTAs")
     for i, n in enumerate(names):
-        v = (t[:, i] - t0) / 1e3
-        print(f"  {n:24s} t(us) min {v.min():7.2f}  p50 {np.median(v):7.2f}  p90 {np.percentile(v, 90):7.2f}  max {v.max():7.2f}")
+        ok = t[:, i] > 0
+        if not ok.any():
+            continue
+        v = (t[ok, i] - t0) / 1e3
+        print(f"  {n:16s} (n={ok.sum():4d}) t(us) min {v.min():7.2f}  p50 {np.median(v):7.2f}  p90 {np.percentile(v, 90):7.2f}  max {v.max():7.2f}")
     for i in range(1, len(names)):
-        d = (t[:, i] - t[:, i - 1]) / 1e3
-        print(f"  dur {names[i - 1]}->{names[i]:14s} p50 {np.median(d):7.2f} p90 {np.percentile(d, 90):7.2f} max {d.max():7.2f}")
+        ok = (t[:, i] > 0) & (t[:, i - 1] > 0)
+        if ok.any():
+            d = (t[ok, i] - t[ok, i - 1]) / 1e3
+            print(f"  dur {names[i - 1]}->{names[i]:14s} p50 {np.median(d):7.2f} p90 {np.percentile(d, 90):7.2f} max {d.max():7.2f}")
 
 
-report(0, ["start", "done"])
-report(1, ["start", "boundary1", "pass done", "resolved", "compacted"])
+report(0, ["start", "streamed", "emitted", "staged", "selected"])
+
+
+def report1():
+    t = buf[1].astype(np.int64)
+    t = t[t[:, 0] > 0]
+    names = {0: "start", 4: "pdl waited", 1: "staged", 5: "level1", 6: "level2", 7: "level3", 2: "radix done",
+             8: "pass A", 9: "pass B", 3: "compacted"}
+    order = [0, 4, 1, 5, 6, 7, 2, 8, 9, 3]
+    prev = None
+    print("\nselect phases (p50 of per-CTA durations, us):")
+    for s_ in order:
+        col = t[:, s_]
+        ok = col > 0
+        if prev is not None and ok.any():
+            d = (col[ok] - t[ok, prev]) / 1e3
+            print(f"  {names[prev]:>12s} -> {names[s_]:12s} p50 {np.median(d):7.2f}  p90 {np.percentile(d, 90):7.2f}  (n={ok.sum()})")
+        if ok.any():
+            prev = s_
 report(2, ["start", "rowids", "loop done", "cluster sync", "merged"])
