@@ -134,9 +134,10 @@ size_t ds_decode_workspace_size(const ds_cache *c, int32_t k);
  *                  16-byte aligned, ZERO-FILLED before its first use; every
  *                  call leaves its synchronisation words zeroed again, so it
  *                  can be reused by later calls on the same stream (not by
- *                  concurrent calls).  It holds per-unit arrival counters and
- *                  ready flags through which the attention of a (b, KV head)
- *                  unit starts as soon as that unit's selection is published.
+ *                  concurrent calls).  It holds the selected index lists,
+ *                  their pool row ids and per-unit ready flags through which
+ *                  the attention of a (b, KV head) unit starts as soon as that
+ *                  unit's selection is published.
  * Errors: DS_ERR_INVALID_ARGUMENT if k < 1 or k > max_seq_len. A sequence
  * with seq_lens[b] == 0 yields out = 0. */
 ds_status ds_decode_attention(const ds_cache *c, const void *q, int32_t k, void *out,

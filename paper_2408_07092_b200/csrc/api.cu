@@ -36,8 +36,6 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 Workspace carve_workspace(const ds_cache *c, int k, void *base) {
   const size_t units = (size_t)c->batch * c->num_kv_heads;
   const size_t kb = align256(units * (size_t)(k > 0 ? k : 0) * sizeof(int32_t));
-  const size_t cand_b = align256(select_workspace_cand(c));
-  const size_t cnt_b = align256(select_workspace_count(c));
   const size_t flag_b = align256(units * sizeof(uint32_t));
   char *p = (char *)base;
   size_t off = 0;
@@ -47,10 +45,6 @@ Workspace carve_workspace(const ds_cache *c, int k, void *base) {
     off += n;
     return q;
   };
-  w.cand = (uint2 *)take(cand_b);
-  w.cand_count = (uint32_t *)take(cnt_b);
-  w.cand_minmax = (uint32_t *)take(2 * cnt_b);
-  w.counter = (uint32_t *)take(flag_b);
   w.ready = (uint32_t *)take(flag_b);
   w.idx = (int32_t *)take(kb);
   w.rowid = (int32_t *)take(kb);
@@ -151,23 +145,18 @@ ds_status ds_decode_attention(const ds_cache *c, const void *q, int32_t k, void 
   if (k < 1 || k > c->max_seq_len || !q || !out || !aligned16(q) || !aligned16(out)) return DS_ERR_INVALID_ARGUMENT;
   Workspace w = carve_workspace(c, k, workspace);
   if (!workspace || workspace_bytes < w.bytes || !aligned16(workspace)) return DS_ERR_WORKSPACE_TOO_SMALL;
-  SelectGeom sg = select_geom(c, k);
+  SelectGeom sg = select_geom(c);
   AttnGeom ag = attn_geom(c, k);
   if (ag.nsplit < 1) return DS_ERR_UNSUPPORTED;
   ScoreParams sc;
   sc.c = make_view(c);
   sc.q = q;
   sc.k = k;
-  sc.cand = w.cand;
-  sc.cand_count = w.cand_count;
-  sc.cand_minmax = w.cand_minmax;
-  sc.counter = w.counter;
   sc.ready = w.ready;
   sc.idx = topk_idx_out ? topk_idx_out : w.idx;
   sc.rowid = w.rowid;
   sc.scores = nullptr;
   sc.chunk = sg.chunk;
-  sc.stage_cap = sg.stage_cap;
   if (launch_score(c, sc, sg, stream) != cudaSuccess) return DS_ERR_CUDA;
   AttnParams ap;
   fill_attn(ap, c, q, w.rowid, k, ag, out);
@@ -179,21 +168,16 @@ ds_status ds_approx_scores(const ds_cache *c, const void *q, float *scores_out, 
   ds_status s = validate_cache(c);
   if (s != DS_OK) return s;
   if (!q || !scores_out || !aligned16(q)) return DS_ERR_INVALID_ARGUMENT;
-  SelectGeom sg = select_geom(c, 1);
+  SelectGeom sg = select_geom(c);
   ScoreParams sc;
   sc.c = make_view(c);
   sc.q = q;
   sc.k = 1;
-  sc.cand = nullptr;
-  sc.cand_count = nullptr;
-  sc.cand_minmax = nullptr;
-  sc.counter = nullptr;
   sc.ready = nullptr;
   sc.idx = nullptr;
   sc.rowid = nullptr;
   sc.scores = scores_out;
   sc.chunk = sg.chunk;
-  sc.stage_cap = 0;
   return cuda_status(launch_score(c, sc, sg, stream));
 }
 

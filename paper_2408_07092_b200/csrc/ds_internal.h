@@ -21,16 +21,11 @@ struct ScoreParams {
   CacheView c;
   const void *q;         // [B][Hq][D]
   int k;
-  uint2 *cand;           // [units][cand_stride]: (order key, token), chunk segments
-  uint32_t *cand_count;  // [units][kMaxChunks]
-  uint32_t *cand_minmax; // [units][kMaxChunks][2] min / max emitted key
-  uint32_t *counter;     // [units] arrivals of the unit's CTAs (0 between calls)
   uint32_t *ready;       // [units] selection published (0 between calls)
   int32_t *idx;          // [units][k] ascending token indices (-1 past k_eff)
   int32_t *rowid;        // [units][k] pool row ids of the same tokens
   float *scores;         // non-null: ds_approx_scores mode (s_hat [units][Smax] only)
-  int chunk;             // tokens per CTA
-  int stage_cap;         // candidates the dynamic smem can stage
+  int chunk;             // tokens per CTA (cluster = nchunks CTAs per unit)
 };
 
 struct AttnParams {
@@ -46,14 +41,11 @@ struct AttnParams {
 
 // Launch-geometry decisions (deterministic functions of the cache shape).
 struct SelectGeom {
-  int chunk, nchunks;  // score CTAs per unit
+  int chunk, nchunks;  // score CTAs per unit (one cluster)
   int threads;
-  size_t score_smem;   // dynamic smem (a chunk's keys / the staged candidates)
-  int stage_cap;
+  size_t score_smem;   // dynamic smem (a chunk's keys + its block-table entries)
 };
-SelectGeom select_geom(const ds_cache *c, int k);
-size_t select_workspace_cand(const ds_cache *c);
-size_t select_workspace_count(const ds_cache *c);
+SelectGeom select_geom(const ds_cache *c);
 
 struct AttnGeom {
   int rows_per_cta, nsplit, threads;
@@ -61,10 +53,9 @@ struct AttnGeom {
 };
 AttnGeom attn_geom(const ds_cache *c, int n_rows);
 
-// Workspace layout: candidates | candidate counts | counters | ready flags | idx | rowid.
+// Workspace layout: ready flags | idx | rowid.
 struct Workspace {
-  uint2 *cand;
-  uint32_t *cand_count, *cand_minmax, *counter, *ready;
+  uint32_t *ready;
   int32_t *idx, *rowid;
   size_t bytes;
 };

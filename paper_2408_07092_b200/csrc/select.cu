@@ -1,101 +1,55 @@
 // select.cu -- a1..a3 of Algorithm 1: label-score GEMV and exact
-// top-k selection, fused in one kernel (score_select_kernel, grid chunks x
-// units, 512 threads; see the kernel's comment for the three phases).
+// top-k selection, fused in one kernel: score_select_kernel, grid
+// (nch, units) with the nch CTAs of a (b, KV head) unit forming one thread-
+// block cluster; each CTA owns a contiguous chunk of tokens.
 //   a1  q_lab[j] = sum_g q[b][hG+g][C[h][j]]      (fp32, g order; reading R3)
 //   a2  s_hat[t] = fma-chain_j(q_lab[j], L[t][j])  (fp32, j ascending, no
 //       1/sqrt(d); reading R2), streamed from the contiguous label cache with
 //       eight 128-bit loads in flight per thread (one row = r*e = 16 B at
-//       r=8 / 16-bit) into a monotone u32 order key (-0 == +0) in smem.
+//       r=8 / 16-bit), kept in shared memory as monotone u32 order keys
+//       (-0 == +0) while a 12-bit histogram of the keys' top bits is built.
+//       s_hat never leaves the chip.
 //   a3  i = argtopk(s_hat, k): exact, ties to the lower index, ascending
-//       (reading R6).  Each chunk emits a candidate superset of its share of
-//       the global top-k; the unit's last-arriving CTA selects exactly among
-//       them (MSB radix 12+12+8 bits, equal keys by token order) and writes
-//       the index list with each token's pool row id.  s_hat never leaves the
-//       chip; the candidates (~k + a histogram bin per chunk) stay in L2.
+//       (reading R6).  The selection is fixed by one boundary pair (kB, tB):
+//       token t is selected  <=>  key > kB  or  (key == kB and t <= tB),
+//       i.e. rank < k in the order (key desc, token asc).  It is found with
+//       cluster barriers and a few KB of DSMEM reads:
+//         S1  cluster histogram of bits 31..20 -> boundary digit D1
+//         L2  one pass over the chunk: keys with digit D1 (a few hundred)
+//             go to a candidate list and a 10-bit histogram of bits 19..10
+//         S2  cluster histogram -> 22-bit boundary prefix P2
+//         S3  the keys with prefix P2 (typically < 10) and per-CTA counts
+//             are exchanged; every CTA ranks those members exactly
+//         S4  exit guard; CTA 0 publishes the unit's ready flag
+//       then each CTA writes its selected tokens, ascending, at its cluster
+//       prefix offset together with their pool row ids (block_table), so the
+//       attention kernel's gathers start after a single load.  If more than
+//       kMaxMembers keys share P2 (massive ties), the last 10 bits and the
+//       token order of equal keys are resolved with two more barriers.
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
 #include "ds_common.cuh"
 #include "ds_internal.h"
 
+namespace cg = cooperative_groups;
+
 namespace ds {
 
-constexpr int kScoreThreads = 512;
-constexpr int kScoreWarps = kScoreThreads / 32;
-constexpr int kScoreUnroll = 8;
-constexpr int kMaxChunks = 16;       // score CTAs per unit
-constexpr int kMaxChunkLen = 16384;  // tokens per score CTA (keys kept in smem)
-constexpr int kMaxDynSmem = 200 * 1024;
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kUnroll = 8;
+constexpr int kMaxChunks = 16;       // CTAs (cluster size) per unit
+constexpr int kMaxChunkLen = 16384;  // tokens per CTA (keys kept in smem)
 constexpr int kMaxR = 256;
-constexpr int kDigitBits = 12;
-constexpr int kBins = 1 << kDigitBits;
-constexpr int kShift1 = 32 - kDigitBits;  // level-1 digit: top 12 key bits
-
-// per-unit stride of the candidate workspace (>= nchunks * chunk for any geometry)
-__host__ __device__ __forceinline__ size_t cand_stride(int smax) {
-  return (size_t)smax + (size_t)kMaxChunks * 256;
-}
-
-// ------------------------------------------------------------ helpers
-// Block-wide exclusive prefix of one u32 per thread (NT threads); *total =
-// sum.  Two shuffle levels (warp, then warp 0 over the warp totals): 2
-// barriers, no serial smem walks.  warp_tot needs NT/32 + 1 entries.
-template <int NT>
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *warp_tot, uint32_t *total) {
-  constexpr int NW = NT / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  __syncthreads();  // warp_tot may still be read by a previous scan
-  if (lane == 31) warp_tot[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    const uint32_t t = lane < NW ? warp_tot[lane] : 0u;
-    uint32_t y = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
-      if (lane >= o) y += z;
-    }
-    if (lane < NW) warp_tot[lane] = y - t;
-    if (lane == NW - 1) warp_tot[NW] = y;
-  }
-  __syncthreads();
-  *total = warp_tot[NW];
-  return warp_tot[warp] + x - v;
-}
-
-// Boundary digit of a histogram bins[nb] (nb a multiple of NT): with `need`
-// keys wanted from the top, the digit d with above(d) < need <= above(d) +
-// bins[d]; every thread gets (d, above(d), bins[d]).
-template <int NT>
-__device__ __forceinline__ void find_boundary(const uint32_t *bins, int nb, uint32_t need, uint32_t *warp_tot,
-                                              uint32_t *state, uint32_t &d, uint32_t &above, uint32_t &cnt) {
-  const int per = nb / NT;  // thread t owns digits nb-1-per*t-j, descending
-  uint32_t s = 0;
-  for (int j = 0; j < per; ++j) s += bins[nb - 1 - per * (int)threadIdx.x - j];
-  uint32_t tot;
-  uint32_t run = block_excl_scan<NT>(s, warp_tot, &tot);
-  for (int j = 0; j < per; ++j) {
-    const int dd = nb - 1 - per * (int)threadIdx.x - j;
-    const uint32_t v = bins[dd];
-    if (run < need && run + v >= need) {
-      state[0] = dd;
-      state[1] = run;
-      state[2] = v;
-    }
-    run += v;
-  }
-  __syncthreads();
-  d = state[0];
-  above = state[1];
-  cnt = state[2];
-  __syncthreads();
-}
+constexpr int kSh1 = 20, kD1 = 4096;  // level-1 digit: key bits 31..20
+constexpr int kSh2 = 10, kD2 = 1024;  // level-2 digit: key bits 19..10
+constexpr int kD3 = 1024;             // level-3 digit: key bits 9..0
+constexpr int kCandCap = 1024;        // level-1 boundary keys listed per CTA
+constexpr int kMaxMembers = 512;      // P2 keys ranked directly (cluster-wide)
+constexpr int kMaxPageRow = 1024;     // block-table entries cached per CTA
+constexpr int kMaxDynSmem = (kMaxChunkLen + 128) * 4 + kMaxPageRow * 4;
 
 // ------------------------------------------------------------------ A
 template <typename T, int R>
@@ -115,460 +69,179 @@ __device__ __forceinline__ float label_score(const T *__restrict__ row, const fl
   return s;
 }
 
-// Candidate sources for the unit's exact selection: staged in shared memory
-// (the usual case) or read in place from the per-chunk segments in global
-// memory (tie-heavy boundaries with more candidates than fit).
-struct StagedSrc {
-  const uint2 *a;
-  __device__ __forceinline__ uint2 get(int s) const { return a[s]; }
-};
-struct GlobalSrc {
-  const uint2 *g;
-  const uint32_t *seg;
-  int chunk;
-  __device__ __forceinline__ uint2 get(int s) const {
-    int q = 0;
-    while ((int)seg[q + 1] <= s) ++q;
-    return __ldcg(g + (size_t)q * chunk + (s - (int)seg[q]));
-  }
-};
-
-struct SelScratch {
-  uint32_t *bins;      // [kBins]
-  uint32_t *warp_tot;  // [NW + 1]
-  uint32_t *state;     // [4]
+struct SelSh {
+  float qlab[kMaxR];
+  uint32_t h1[kD1];  // level-1 histogram (read remotely S1..S2); later the level-3 one
+  uint32_t c1[64];   // 64-bin coarse sums of h1 (remote S1..S2)
+  uint32_t h2[kD2];  // level-2 histogram (remote S2..S3)
+  uint32_t c2[32];   // coarse sums of h2 (remote S2..S3)
+  uint2 cand[kCandCap];         // (key, token) with digit1 == D1
+  uint2 members[kMaxMembers];   // (key, token) with prefix P2 (remote S3..S4)
+  uint2 gathered[kMaxMembers];
+  uint32_t gtm[kMaxChunkLen / 32];  // per 32-token group: digit1 > D1 (>= D1 if taken whole)
+  uint32_t eqm[kMaxChunkLen / 32];  // per 32-token group: digit1 == D1 (not whole)
+  uint32_t wcnt[kWarps];  // per-warp scratch counts
+  uint32_t cnt[4];        // [0] #digit1 > D1 (or >= if whole), [1] #(digit1 == D1, prefix > P2), [3] total
+  uint32_t state[8];
+  uint32_t ncand, nmem, lower_sel, pad;
 };
 
-// Exact top-k_eff of T candidates (ascending token order) with ties to the
-// lower index: MSB radix over 12 + 12 + 8 key bits for the k-th key, then
-// one ordered pass writes the selected tokens (ascending) and their pool row
-// ids.  NT threads.
-template <int NT, class Src>
-__device__ __forceinline__ void select_core(const Src &src, int T, uint32_t keff, const SelScratch &sc,
-                                            int32_t *idx_out, int32_t *rid_out, const CacheView &c, int b,
-                                            int h) {
-  constexpr int NW = NT / 32;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t need = keff, prefix = 0, mask = 0;
-  bool whole = false;  // the boundary bin is taken entirely
-  for (int lv = 0; lv < 3 && !whole; ++lv) {
-    const int sh = lv == 0 ? 20 : (lv == 1 ? 8 : 0), nb = lv < 2 ? 4096 : 256;
-    const uint32_t wm = (uint32_t)nb - 1u;
-    const int nbz = nb < NT ? NT : nb;
-    for (int i = tid; i < nbz; i += NT) sc.bins[i] = 0;
-    __syncthreads();
-#pragma unroll 4
-    for (int s = tid; s < T; s += NT) {
-      const uint32_t key = src.get(s).x;
-      if ((key & mask) == prefix) atomicAdd(&sc.bins[(key >> sh) & wm], 1u);
+// Warp 0: boundary of a histogram held NPL bins per lane, bins in
+// descending order hi_bin - NPL*lane - j.  With `base` keys above the
+// first bin and `need` wanted from the top, returns the bin d with
+// above(d) < need <= above(d) + cnt(d).
+template <int NPL>
+struct Boundary {
+  int bin;
+  uint32_t above, cnt;
+};
+template <int NPL>
+__device__ __forceinline__ Boundary<NPL> warp_boundary(const uint32_t (&v)[NPL], int hi_bin, uint32_t base,
+                                                       uint32_t need) {
+  const int lane = threadIdx.x & 31;
+  uint32_t tot = 0;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) tot += v[j];
+  uint32_t incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  uint32_t run = base + incl - tot;
+  int hit = -1;
+  uint32_t ha = 0, hc = 0;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    if (hit < 0 && run < need && run + v[j] >= need) {
+      hit = j;
+      ha = run;
+      hc = v[j];
     }
-    __syncthreads();
-    uint32_t d, above, cnt;
-    find_boundary<NT>(sc.bins, nbz, need, sc.warp_tot, sc.state, d, above, cnt);
-    need -= above;
-    prefix |= d << sh;
-    mask |= wm << sh;
-    whole = cnt == need;
+    run += v[j];
   }
-  // ordered selection: masked key > prefix, or == prefix and (the whole bin
-  // is taken, or it is among the first `need` equal keys in token order)
-  int per = (T + NW - 1) / NW;
-  per = (per + 31) & ~31;
-  const int w0 = min(warp * per, T), w1 = min(w0 + per, T);
-  const uint32_t lt = lanemask_lt();
-  uint32_t tot, eq_base = 0;
-  if (!whole) {
-    uint32_t weq = 0;
-#pragma unroll 4
-    for (int base = w0; base < w1; base += 32) {
-      const int s = base + lane;
-      weq += __popc(__ballot_sync(0xffffffffu, s < w1 && (src.get(s).x & mask) == prefix));
-    }
-    eq_base = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? weq : 0u, sc.warp_tot, &tot), 0);
-  }
-  uint32_t wtake = 0, run = eq_base;
-#pragma unroll 4
-  for (int base = w0; base < w1; base += 32) {
-    const int s = base + lane;
-    const uint32_t km = s < w1 ? (src.get(s).x & mask) : 0u;
-    const bool gt = s < w1 && km > prefix, eq = s < w1 && km == prefix;
-    const uint32_t em = __ballot_sync(0xffffffffu, eq);
-    const bool take = gt || (eq && (whole || run + __popc(em & lt) < need));
-    wtake += __popc(__ballot_sync(0xffffffffu, take));
-    run += __popc(em);
-  }
-  uint32_t pos = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? wtake : 0u, sc.warp_tot, &tot), 0);
-  run = eq_base;
-  const int32_t *bt = c.block_table + (size_t)b * c.maxp;
-  const bool pow2 = (c.P & (c.P - 1)) == 0;
-  const int psh = __ffs(c.P) - 1;
-#pragma unroll 2
-  for (int base = w0; base < w1; base += 32) {
-    const int s = base + lane;
-    uint2 e = make_uint2(0u, 0u);
-    if (s < w1) e = src.get(s);
-    const uint32_t km = e.x & mask;
-    const bool gt = s < w1 && km > prefix, eq = s < w1 && km == prefix;
-    const uint32_t em = __ballot_sync(0xffffffffu, eq);
-    const bool take = gt || (eq && (whole || run + __popc(em & lt) < need));
-    const uint32_t tm = __ballot_sync(0xffffffffu, take);
-    if (take) {
-      const uint32_t o = pos + __popc(tm & lt);
-      const int t = (int)e.y;
-      const int pg = pow2 ? (t >> psh) : t / c.P;
-      const int sl = pow2 ? (t & (c.P - 1)) : t - pg * c.P;
-      idx_out[o] = t;
-      rid_out[o] = (int32_t)(((uint32_t)__ldg(bt + pg) * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P + (uint32_t)sl);
-    }
-    pos += __popc(tm);
-    run += __popc(em);
-  }
+  const uint32_t m = __ballot_sync(0xffffffffu, hit >= 0);
+  const int src = m ? __ffs(m) - 1 : 31;
+  Boundary<NPL> r;
+  r.bin = hi_bin - NPL * src - __shfl_sync(0xffffffffu, hit < 0 ? 0 : hit, src);
+  r.above = __shfl_sync(0xffffffffu, ha, src);
+  r.cnt = __shfl_sync(0xffffffffu, hc, src);
+  return r;
 }
 
-// select_core for candidates staged in shared memory (16-B aligned, padded
-// by 4 entries): warp w owns 128-candidate blocks; lane l handles candidates
-// 4l..4l+3 of a block (two 128-bit loads), prefix sums by warp shuffles.
-template <int NT>
-__device__ __forceinline__ void select_core_staged(const uint2 *cand, int T, uint32_t keff, const SelScratch &sc,
-                                                   int32_t *idx_out, int32_t *rid_out, const CacheView &c, int b,
-                                                   int h) {
-  constexpr int NW = NT / 32;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int per = (T + NW - 1) / NW;
-  per = (per + 127) & ~127;
-  const int w0 = min(warp * per, T), w1 = min(w0 + per, T);
-  auto load4 = [&](int base, uint32_t (&k)[4], uint32_t (&t)[4]) {
-    const uint4 a = *reinterpret_cast<const uint4 *>(cand + base + 4 * lane);
-    const uint4 bq = *reinterpret_cast<const uint4 *>(cand + base + 4 * lane + 2);
-    k[0] = a.x; t[0] = a.y; k[1] = a.z; t[1] = a.w;
-    k[2] = bq.x; t[2] = bq.y; k[3] = bq.z; t[3] = bq.w;
-  };
-  auto warp_excl = [&](uint32_t v, uint32_t &total) {
-    uint32_t x = v;
+// Cluster-wide boundary over a histogram of 64*64 (NC=64, coarse sums in c)
+// or 32*32 (NC=32) bins, each CTA holding its own copy; warp 0 only.
+template <int NC>
+__device__ __forceinline__ Boundary<NC / 32> cluster_boundary(cg::cluster_group &cluster, int nch, uint32_t *h,
+                                                              uint32_t *cs, uint32_t need) {
+  constexpr int NPL = NC / 32;
+  const int lane = threadIdx.x & 31;
+  uint32_t v[NPL];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    total = __shfl_sync(0xffffffffu, x, 31);
-    return x - v;
-  };
-  uint32_t need = keff, prefix = 0, mask = 0;
-  bool whole = false;
-  for (int lv = 0; lv < 3 && !whole; ++lv) {
-    const int sh = lv == 0 ? 20 : (lv == 1 ? 8 : 0), nb = lv < 2 ? 4096 : 256;
-    const uint32_t wm = (uint32_t)nb - 1u;
-    const int nbz = nb < NT ? NT : nb;
-    for (int i = tid; i < nbz; i += NT) sc.bins[i] = 0;
-    __syncthreads();
-    for (int base = w0; base < w1; base += 128) {
-      uint32_t k[4], t[4];
-      load4(base, k, t);
+  for (int j = 0; j < NPL; ++j) v[j] = 0;
+  for (int cr = 0; cr < nch; ++cr) {
+    const uint32_t *rc = cluster.map_shared_rank(cs, cr);
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (base + 4 * lane + e < w1 && (k[e] & mask) == prefix) atomicAdd(&sc.bins[(k[e] >> sh) & wm], 1u);
-    }
-    __syncthreads();
-    uint32_t d, above, cnt;
-    find_boundary<NT>(sc.bins, nbz, need, sc.warp_tot, sc.state, d, above, cnt);
-    need -= above;
-    prefix |= d << sh;
-    mask |= wm << sh;
-    whole = cnt == need;
+    for (int j = 0; j < NPL; ++j) v[j] += rc[NC - 1 - NPL * lane - j];
   }
-  uint32_t tot, eq_base = 0;
-  if (!whole) {  // equal keys beyond the first `need` are dropped: their ordinals
-    uint32_t weq = 0;
-    for (int base = w0; base < w1; base += 128) {
-      uint32_t k[4], t[4];
-      load4(base, k, t);
+  const Boundary<NPL> cb = warp_boundary<NPL>(v, NC - 1, 0u, need);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) weq += base + 4 * lane + e < w1 && (k[e] & mask) == prefix;
-    }
+  for (int j = 0; j < NPL; ++j) v[j] = 0;
+  for (int cr = 0; cr < nch; ++cr) {
+    const uint32_t *rf = cluster.map_shared_rank(h, cr) + cb.bin * NC;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) weq += __shfl_xor_sync(0xffffffffu, weq, o);
-    eq_base = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? weq : 0u, sc.warp_tot, &tot), 0);
+    for (int j = 0; j < NPL; ++j) v[j] += rf[NC - 1 - NPL * lane - j];
   }
-  // per lane: take flags for its 4 candidates (gt, or eq within the first `need`)
-  auto takes = [&](int base, const uint32_t (&k)[4], uint32_t &run, bool (&tk)[4]) {
-    bool eq[4];
-    uint32_t ne = 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const bool in = base + 4 * lane + e < w1;
-      const uint32_t km = k[e] & mask;
-      eq[e] = in && km == prefix;
-      tk[e] = in && km > prefix;
-      ne += eq[e];
-    }
-    uint32_t etot;
-    uint32_t eo = run + (whole ? 0u : warp_excl(ne, etot));
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      tk[e] = tk[e] || (eq[e] && (whole || eo < need));
-      eo += eq[e];
-    }
-    if (!whole) run += etot;
-  };
-  uint32_t wtake = 0, run = eq_base;
-  for (int base = w0; base < w1; base += 128) {
-    uint32_t k[4], t[4];
-    bool tk[4];
-    load4(base, k, t);
-    takes(base, k, run, tk);
-    wtake += tk[0] + tk[1] + tk[2] + tk[3];
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) wtake += __shfl_xor_sync(0xffffffffu, wtake, o);
-  uint32_t pos = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? wtake : 0u, sc.warp_tot, &tot), 0);
-  run = eq_base;
-  const int32_t *bt = c.block_table + (size_t)b * c.maxp;
-  const bool pow2 = (c.P & (c.P - 1)) == 0;
-  const int psh = __ffs(c.P) - 1;
-  for (int base = w0; base < w1; base += 128) {
-    uint32_t k[4], t[4];
-    bool tk[4];
-    load4(base, k, t);
-    takes(base, k, run, tk);
-    const uint32_t nt = tk[0] + tk[1] + tk[2] + tk[3];
-    uint32_t ttot;
-    uint32_t o = pos + warp_excl(nt, ttot);
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-      if (tk[e]) {
-        const int tok = (int)t[e];
-        const int pg = pow2 ? (tok >> psh) : tok / c.P;
-        const int sl = pow2 ? (tok & (c.P - 1)) : tok - pg * c.P;
-        idx_out[o] = tok;
-        rid_out[o] = (int32_t)(((uint32_t)__ldg(bt + pg) * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P +
-                               (uint32_t)sl);
-        ++o;
-      }
-    pos += ttot;
-  }
+  return warp_boundary<NPL>(v, cb.bin * NC + NC - 1, cb.above, need);
 }
 
-// Exact top-k of T staged candidates (ascending token order), fast path:
-// level 1 = 4096 linear fp32 bins over [lo, hi] (the candidates' key range),
-// so the boundary bin holds only a few keys; the boundary is found by one warp
-// over a 64-bin coarse then a 64-bin fine scan; the boundary bin's members are
-// ranked exactly by (key desc, token asc) by one warp; one ordered pass writes
-// the selected tokens and their pool row ids.  Returns false (nothing
-// written) when the boundary bin is too crowded (ties): the caller then runs
-// the generic radix path.
-constexpr int kMaxMembers = 256;
-struct FastScratch {
-  uint32_t *fine;      // [4096]
-  uint32_t *coarse;    // [64]
-  uint2 *members;      // [kMaxMembers] (key, slot)
-  uint32_t *selbits;   // [T/32 + 1] selected boundary members, by slot
-  uint32_t *warp_tot;  // [NW + 1]
-  uint32_t *state;     // [8]
-};
-
-template <int NT>
-__device__ __forceinline__ bool select_fast(const uint2 *cand, int T, uint32_t keff, uint32_t lo_key,
-                                            uint32_t hi_key, const FastScratch &sc, int32_t *idx_out,
-                                            int32_t *rid_out, const int32_t *btrow, const CacheView &c, int h) {
-  constexpr int NW = NT / 32;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const float lo = key_to_float(lo_key), hi = key_to_float(hi_key);
-  const float scale = 4096.0f / (hi - lo);
-  auto binof = [&](uint32_t key) -> int {
-    const float x = fminf(fmaxf((key_to_float(key) - lo) * scale, 0.0f), 4095.0f);
-    return (int)x;
-  };
-  for (int i = tid; i < 4096; i += NT) sc.fine[i] = 0;
-  if (tid < 64) sc.coarse[tid] = 0;
-  for (int i = tid; i <= T / 32; i += NT) sc.selbits[i] = 0;
-  if (tid == 0) sc.state[4] = 0;
-  __syncthreads();
-#pragma unroll 4
-  for (int s = tid; s < T; s += NT) {
-    const int bn = binof(cand[s].x);
-    atomicAdd(&sc.fine[bn], 1u);
-    atomicAdd(&sc.coarse[bn >> 6], 1u);
-  }
-  __syncthreads();
-  if (warp == 0) {  // coarse then fine boundary, descending bins
-    uint32_t above = 0;
-    int cb = 0;
-    {
-      const uint32_t a = sc.coarse[63 - 2 * lane], bq = sc.coarse[62 - 2 * lane];
-      uint32_t incl = a + bq;
+// coarse sums: cs[i] = sum of h[i*NC .. i*NC+NC-1] for NC*NC bins (all threads)
+template <int NC>
+__device__ __forceinline__ void coarse_sums(const uint32_t *h, uint32_t *cs) {
+  constexpr int kPer = NC * NC / kThreads;  // bins per thread: 8 (NC=64) or 2 (NC=32)
+  constexpr int kLanes = NC / kPer;         // lanes per coarse bin: 8 or 16
+  const int tid = threadIdx.x;
+  uint32_t v = 0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const uint32_t ex = incl - a - bq;
-      const bool h0 = ex < keff && ex + a >= keff;
-      const bool h1 = !h0 && ex + a < keff && ex + a + bq >= keff;
-      const uint32_t m = __ballot_sync(0xffffffffu, h0 || h1);
-      const int src = __ffs(m) - 1;
-      const bool sh1 = __shfl_sync(0xffffffffu, h1, src);
-      cb = 63 - 2 * src - (sh1 ? 1 : 0);
-      above = __shfl_sync(0xffffffffu, sh1 ? ex + a : ex, src);
-    }
-    {
-      const int f0 = cb * 64;
-      const uint32_t a = sc.fine[f0 + 63 - 2 * lane], bq = sc.fine[f0 + 62 - 2 * lane];
-      uint32_t incl = a + bq;
+  for (int j = 0; j < kPer; ++j) v += h[tid * kPer + j];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const uint32_t ex = above + incl - a - bq;
-      const bool h0 = ex < keff && ex + a >= keff;
-      const bool h1 = !h0 && ex + a < keff && ex + a + bq >= keff;
-      const uint32_t m = __ballot_sync(0xffffffffu, h0 || h1);
-      const int src = __ffs(m) - 1;
-      if (lane == src) {
-        sc.state[0] = f0 + 63 - 2 * lane - (h1 ? 1 : 0);
-        sc.state[1] = h1 ? ex + a : ex;
-        sc.state[2] = h1 ? bq : a;
-      }
-    }
-  }
-  __syncthreads();
-  const int b1 = (int)sc.state[0];
-  const uint32_t need = keff - sc.state[1], cnt = sc.state[2];
-  const bool whole = cnt == need;
-  if (!whole) {
-    if (cnt > (uint32_t)kMaxMembers) return false;
-    // members of the boundary bin -> list, ranked exactly by warp 0
-#pragma unroll 4
-    for (int s = tid; s < T; s += NT) {
-      const uint32_t key = cand[s].x;
-      if (binof(key) == b1) sc.members[atomicAdd(&sc.state[4], 1u)] = make_uint2(key, (uint32_t)s);
-    }
-    __syncthreads();
-    if (warp == 0) {
-      const int m = (int)sc.state[4];
-      for (int i = lane; i < m; i += 32) {
-        const uint2 me = sc.members[i];
-        uint32_t rank = 0;
-        for (int j = 0; j < m; ++j) {
-          const uint2 o = sc.members[j];
-          rank += (o.x > me.x) || (o.x == me.x && o.y < me.y);  // slot order == token order
-        }
-        if (rank < need) atomicOr(&sc.selbits[me.y >> 5], 1u << (me.y & 31));
-      }
-    }
-    __syncthreads();
-  }
-  // ---- ordered pass: warp w owns a contiguous slot range
-  int per = (T + NW - 1) / NW;
-  per = (per + 31) & ~31;
-  const int w0 = min(warp * per, T), w1 = min(w0 + per, T);
-  auto take = [&](int s, uint32_t key) {
-    const int bn = binof(key);
-    return bn > b1 || (bn == b1 && (whole || ((sc.selbits[s >> 5] >> (s & 31)) & 1u)));
-  };
-  uint32_t wt = 0;
-#pragma unroll 4
-  for (int base = w0; base < w1; base += 32) {
-    const int s = base + lane;
-    wt += __popc(__ballot_sync(0xffffffffu, s < w1 && take(s, cand[s].x)));
-  }
-  uint32_t tot;
-  uint32_t pos = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? wt : 0u, sc.warp_tot, &tot), 0);
-  const uint32_t lt = lanemask_lt();
-  const bool pow2 = (c.P & (c.P - 1)) == 0;
-  const int psh = __ffs(c.P) - 1;
-#pragma unroll 2
-  for (int base = w0; base < w1; base += 32) {
-    const int s = base + lane;
-    uint2 e = make_uint2(0u, 0u);
-    if (s < w1) e = cand[s];
-    const bool tk = s < w1 && take(s, e.x);
-    const uint32_t tm = __ballot_sync(0xffffffffu, tk);
-    if (tk) {
-      const uint32_t o = pos + __popc(tm & lt);
-      const int t = (int)e.y;
-      const int pg = pow2 ? (t >> psh) : t / c.P;
-      const int sl = pow2 ? (t & (c.P - 1)) : t - pg * c.P;
-      idx_out[o] = t;
-      rid_out[o] = (int32_t)(((uint32_t)btrow[pg] * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P + (uint32_t)sl);
-    }
-    pos += __popc(tm);
-  }
-  return true;
+  for (int o = 1; o < kLanes; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((tid & (kLanes - 1)) == 0) cs[tid / kLanes] = v;
 }
 
-// Fused a1 + a2 + a3.  Grid (chunks, units), kScoreThreads threads.
-//   1. stream this chunk's label rows -> keys (smem) + 12-bit digit histogram
-//   2. emit, in token order, every token whose digit is >= the digit bounding
-//      the chunk's local top-k: a superset of the chunk's share of the unit's
-//      global top-k (any global top-k token is in its chunk's top-k)
-//   3. the last CTA of the unit to arrive (global counter) selects exactly
-//      among the unit's candidates, writes the index list and row ids, resets
-//      the counter and publishes ready[unit] for the attention kernel
-// counter[] and ready[] are zero between calls (zero-filled workspace on first
-// use; restored by the last arriver and by the attention kernel).
 template <typename T, int R>
-__global__ void __launch_bounds__(kScoreThreads, 2) score_select_kernel(ScoreParams p) {
-  extern __shared__ __align__(16) uint32_t keys[];  // [chunk] order keys; then staged candidates
-  __shared__ float qlab[kMaxR];
-  __shared__ __align__(16) uint32_t hist[kBins];
-  __shared__ uint32_t warp_tot[kScoreWarps + 1], state[8], seg[kMaxChunks + 1];
-  __shared__ uint32_t coarse[64], mm[2];
-  __shared__ __align__(16) uint2 members[kMaxMembers];
-  __shared__ int last;
+__global__ void __launch_bounds__(kThreads, 2) score_select_kernel(ScoreParams p) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int nch = (int)cluster.num_blocks(), crank = (int)cluster.block_rank();
+  extern __shared__ __align__(16) uint32_t keys[];  // [chunk + 128] order keys, then the page row
+  __shared__ SelSh sh;
   const CacheView &c = p.c;
-  const int unit = blockIdx.y, part = blockIdx.x;
+  const int unit = blockIdx.y;
   const int b = unit / c.Hkv, h = unit - (unit / c.Hkv) * c.Hkv;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = c.seq_lens[b];
-  const int t0 = part * p.chunk;
-  const int nloc = min(p.chunk, n - t0);
-  const int r = R > 0 ? R : c.r;
   const int keff = min(p.k, n);
-  const int nparts = (n + p.chunk - 1) / p.chunk;
+  const int t0 = crank * p.chunk;
+  const int nloc = max(0, min(p.chunk, n - t0));
+  const int r = R > 0 ? R : c.r;
+  int32_t *idx_out = p.idx ? p.idx + (size_t)unit * p.k : nullptr;
+  int32_t *rid_out = p.rowid ? p.rowid + (size_t)unit * p.k : nullptr;
+  int32_t *btrow = reinterpret_cast<int32_t *>(keys + p.chunk + 128);  // pages of this chunk
+  const int pg0 = t0 / c.P;
+  const bool bt_cached = p.chunk / c.P + 2 <= kMaxPageRow;
+  const int32_t *bt = c.block_table + (size_t)b * c.maxp;
   DS_TRACE_AT(0, 0);
-  for (int i = tid; i < kBins; i += kScoreThreads) hist[i] = 0;
   pdl_wait();  // the label rows may come from the preceding append
   pdl_trigger();
+  // (every branch below is uniform over the cluster: n, k, p.scores are)
   if (n <= 0) {  // empty sequence: nothing selected (the attention writes zeros)
-    if (part == 0 && !p.scores)
-      for (int i = tid; i < p.k; i += kScoreThreads) {
-        p.idx[(size_t)unit * p.k + i] = -1;
-        p.rowid[(size_t)unit * p.k + i] = -1;
+    if (crank == 0 && idx_out)
+      for (int i = tid; i < p.k; i += kThreads) {
+        idx_out[i] = -1;
+        rid_out[i] = -1;
       }
     return;
   }
-  if (nloc <= 0) return;
-  for (int j = tid; j < r; j += kScoreThreads) {  // a1
+  // ---- a1 + this chunk's block-table entries (issued early) + zeroing
+  const int npg = nloc > 0 ? (t0 + nloc - 1) / c.P - pg0 + 1 : 0;
+  if (!p.scores && bt_cached)
+    for (int i = tid; i < npg; i += kThreads) btrow[i] = __ldg(bt + pg0 + i);
+  for (int j = tid; j < r; j += kThreads) {
     const T *qb = (const T *)p.q + ((size_t)b * c.Hq + (size_t)h * c.G) * c.D;
     const int ch = c.C[(size_t)h * c.r + j];
     float s = 0.0f;
     for (int g = 0; g < c.G; ++g) s = s + Elem<T>::to_f(qb[(size_t)g * c.D + ch]);
-    qlab[j] = s;
+    sh.qlab[j] = s;
+  }
+  for (int i = tid; i < kD1; i += kThreads) sh.h1[i] = 0;
+  for (int i = tid; i < kD2; i += kThreads) sh.h2[i] = 0;
+  if (tid < kWarps) sh.wcnt[tid] = 0;
+  if (tid == 0) {
+    sh.ncand = 0;
+    sh.nmem = 0;
+    sh.lower_sel = 0;
   }
   __syncthreads();
   float ql[R > 0 ? R : 1];
   if constexpr (R > 0) {
 #pragma unroll
-    for (int j = 0; j < R; ++j) ql[j] = qlab[j];
+    for (int j = 0; j < R; ++j) ql[j] = sh.qlab[j];
   }
-  const float *qs = R > 0 ? ql : qlab;
+  const float *qs = R > 0 ? ql : sh.qlab;
   const T *lab = (const T *)c.label + (((size_t)b * c.Hkv + h) * c.Smax + t0) * (size_t)c.r;
-
   if (p.scores) {  // diagnostics entry (ds_approx_scores): s_hat to HBM
     float *so = p.scores + (size_t)unit * c.Smax + t0;
-    for (int i = tid; i < nloc; i += kScoreThreads) so[i] = label_score<T, R>(lab + (size_t)i * r, qs, r);
+    for (int i = tid; i < nloc; i += kThreads) so[i] = label_score<T, R>(lab + (size_t)i * r, qs, r);
     return;
   }
-  // ---- a2: stream the label: keys + digit histogram
+  // ---- a2: stream the label -> keys + level-1 histogram
   int i0 = tid;
   if constexpr (R > 0 && R * sizeof(T) == 16) {
-    constexpr int U = kScoreUnroll;
-    for (; i0 + (U - 1) * kScoreThreads < nloc; i0 += U * kScoreThreads) {
+    constexpr int U = kUnroll;
+    for (; i0 + (U - 1) * kThreads < nloc; i0 += U * kThreads) {
       uint4 v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        v[u] = __ldg(reinterpret_cast<const uint4 *>(lab) + (size_t)(i0 + u * kScoreThreads));
+      for (int u = 0; u < U; ++u) v[u] = __ldg(reinterpret_cast<const uint4 *>(lab) + (size_t)(i0 + u * kThreads));
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const T *e = reinterpret_cast<const T *>(&v[u]);
@@ -576,236 +249,391 @@ __global__ void __launch_bounds__(kScoreThreads, 2) score_select_kernel(ScorePar
 #pragma unroll
         for (int j = 0; j < R; ++j) s = fmaf(ql[j], Elem<T>::to_f(e[j]), s);
         const uint32_t k0 = order_key(s);
-        keys[i0 + u * kScoreThreads] = k0;
-        atomicAdd(&hist[k0 >> kShift1], 1u);
+        keys[i0 + u * kThreads] = k0;
+        atomicAdd(&sh.h1[k0 >> kSh1], 1u);
       }
     }
   }
-  for (int i = i0; i < nloc; i += kScoreThreads) {
+  for (int i = i0; i < nloc; i += kThreads) {
     const uint32_t k0 = order_key(label_score<T, R>(lab + (size_t)i * r, qs, r));
     keys[i] = k0;
-    atomicAdd(&hist[k0 >> kShift1], 1u);
+    atomicAdd(&sh.h1[k0 >> kSh1], 1u);
   }
-  __syncthreads();
   DS_TRACE_AT(0, 1);
 
-  // ---- local candidates (ordered emission; warp w owns a contiguous range)
-  uint32_t dmin = 0;
-  if (keff < nloc) {
-    uint32_t above, cnt;
-    find_boundary<kScoreThreads>(hist, kBins, (uint32_t)keff, warp_tot, state, dmin, above, cnt);
-  }
-  {
-    // warp w owns 128-token blocks [w0, w1); lane l holds tokens 4l..4l+3 of
-    // a block (one 128-bit smem load); positions by warp-shuffle prefix sums
-    int per = (nloc + kScoreWarps - 1) / kScoreWarps;
-    per = (per + 127) & ~127;
-    const int w0 = min(warp * per, nloc), w1 = min(w0 + per, nloc);
-    uint32_t mine = 0, kmin = 0xffffffffu, kmax = 0u;
-    if (tid == 0) {
-      mm[0] = 0xffffffffu;
-      mm[1] = 0u;
-    }
-#pragma unroll 2
-    for (int base = w0; base < w1; base += 128) {
-      const int i = base + 4 * lane;
-      const uint4 kv = *reinterpret_cast<const uint4 *>(keys + i);
-      const uint32_t kk[4] = {kv.x, kv.y, kv.z, kv.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (i + e < w1 && (kk[e] >> kShift1) >= dmin) {
-          ++mine;
-          kmin = min(kmin, kk[e]);
-          kmax = max(kmax, kk[e]);
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mine += __shfl_xor_sync(0xffffffffu, mine, o);
-      kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-      kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-    }
-    if (lane == 0) {
-      atomicMin(&mm[0], kmin);
-      atomicMax(&mm[1], kmax);
-    }
-    uint32_t tot;
-    uint32_t pos = __shfl_sync(0xffffffffu, block_excl_scan<kScoreThreads>(lane == 0 ? mine : 0u, warp_tot, &tot), 0);
-    uint2 *out = p.cand + (size_t)unit * cand_stride(c.Smax) + (size_t)part * p.chunk;
-#pragma unroll 2
-    for (int base = w0; base < w1; base += 128) {
-      const int i = base + 4 * lane;
-      const uint4 kv = *reinterpret_cast<const uint4 *>(keys + i);
-      const uint32_t kk[4] = {kv.x, kv.y, kv.z, kv.w};
-      bool sel[4];
-      uint32_t cnt = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        sel[e] = i + e < w1 && (kk[e] >> kShift1) >= dmin;
-        cnt += sel[e];
-      }
-      uint32_t incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      uint32_t o = pos + incl - cnt;
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (sel[e]) out[o++] = make_uint2(kk[e], (uint32_t)(t0 + i + e));
-      pos += __shfl_sync(0xffffffffu, incl, 31);
-    }
+  const bool pow2 = (c.P & (c.P - 1)) == 0;
+  const int psh = __ffs(c.P) - 1;
+  auto rowid_of = [&](int t) -> int32_t {
+    const int pg = pow2 ? (t >> psh) : t / c.P;
+    const int sl = t - pg * c.P;
+    const int32_t page = bt_cached ? btrow[pg - pg0] : __ldg(bt + pg);
+    return (int32_t)(((uint32_t)page * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P + (uint32_t)sl);
+  };
+  // warp ranges: warp w owns local tokens [w0, w1), a multiple of 128 long
+  int per = (nloc + kWarps - 1) / kWarps;
+  per = (per + 127) & ~127;
+  const int w0 = min(warp * per, nloc), w1 = min(w0 + per, nloc);
+
+  // every token selected (k >= n): ascending identity
+  if (keff >= n) {
     __syncthreads();
-    if (tid == 0) {
-      p.cand_count[unit * kMaxChunks + part] = tot;
-      p.cand_minmax[(unit * kMaxChunks + part) * 2] = mm[0];
-      p.cand_minmax[(unit * kMaxChunks + part) * 2 + 1] = mm[1];
+    if (crank == 0)
+      for (int i = n + tid; i < p.k; i += kThreads) {
+        idx_out[i] = -1;
+        rid_out[i] = -1;
+      }
+    for (int i = tid; i < nloc; i += kThreads) {
+      idx_out[t0 + i] = t0 + i;
+      rid_out[t0 + i] = rowid_of(t0 + i);
+    }
+    cluster.sync();
+    if (crank == 0 && tid == 0) {
+      __threadfence();
+      atomicExch(p.ready + unit, 1u);
+    }
+    return;
+  }
+  if (crank == 0)  // positions >= k_eff
+    for (int i = keff + tid; i < p.k; i += kThreads) {
+      idx_out[i] = -1;
+      rid_out[i] = -1;
+    }
+  __syncthreads();
+  coarse_sums<64>(sh.h1, sh.c1);
+
+  // ---- S1: level-1 boundary digit D1
+  cluster.sync();
+  if (warp == 0) {
+    const Boundary<2> d1 = cluster_boundary<64>(cluster, nch, sh.h1, sh.c1, (uint32_t)keff);
+    if (lane == 0) {
+      sh.state[0] = (uint32_t)d1.bin;
+      sh.state[1] = d1.above;
+      sh.state[2] = d1.cnt;
     }
   }
+  __syncthreads();
+  const uint32_t D1 = sh.state[0];
+  const uint32_t need1 = (uint32_t)keff - sh.state[1];
+  const bool whole1 = sh.state[2] == need1;
+  const bool ovf = sh.h1[D1] > (uint32_t)kCandCap;  // my D1 keys do not fit the list
   DS_TRACE_AT(0, 2);
 
-  // ---- arrival: the unit's last CTA performs the selection
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();  // release this CTA's candidates
-    last = atomicAdd(p.counter + unit, 1u) == (uint32_t)(nparts - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();  // acquire the other chunks' candidates
-  if (tid == 0) {
-    uint32_t o = 0, lo = 0xffffffffu, hi = 0u;
-    for (int q = 0; q < nparts; ++q) {
-      seg[q] = o;
-      o += __ldcg(p.cand_count + unit * kMaxChunks + q);
-      lo = min(lo, __ldcg(p.cand_minmax + (unit * kMaxChunks + q) * 2));
-      hi = max(hi, __ldcg(p.cand_minmax + (unit * kMaxChunks + q) * 2 + 1));
-    }
-    seg[nparts] = o;
-    mm[0] = lo;
-    mm[1] = hi;
-  }
-  __syncthreads();
-  const int ncand = (int)seg[nparts];
-  const uint2 *gc = p.cand + (size_t)unit * cand_stride(c.Smax);
-  int32_t *idx_out = p.idx + (size_t)unit * p.k;
-  int32_t *rid_out = p.rowid + (size_t)unit * p.k;
-  for (int i = keff + tid; i < p.k; i += kScoreThreads) {  // positions >= k_eff
-    idx_out[i] = -1;
-    rid_out[i] = -1;
-  }
-  const SelScratch scr{hist, warp_tot, state};
-  uint2 *stage = reinterpret_cast<uint2 *>(keys);  // the keys are no longer needed
-  int32_t *btrow = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(keys) + (size_t)p.stage_cap * 8);
-  uint32_t *selbits = reinterpret_cast<uint32_t *>(btrow + c.maxp);
-  bool done = false;
-  if (ncand + 128 <= p.stage_cap) {  // vector loads read up to 127 entries past the end
-    // the block-table row (row ids) and every chunk's candidates: each thread
-    // issues a batch of loads into registers before storing any of them, so
-    // the L2 round trips overlap instead of serialising on the smem stores
-    {
-      const int np = (n + c.P - 1) / c.P;
-      const int32_t *bt = c.block_table + (size_t)b * c.maxp;
-      constexpr int BU = 8;
-      for (int i0 = tid; i0 < np; i0 += BU * kScoreThreads) {
-        int32_t v[BU];
+  // ---- L2: per 32-token group, ballot masks of digit1 > D1 (>= D1 when D1
+  // is taken whole) and digit1 == D1; the D1 keys (a few hundred) go to the
+  // candidate list and the level-2 histogram
+  const uint32_t lt = lanemask_lt();
+  {
+    uint32_t g = 0;
+    for (int base = w0; base < w1; base += 128) {
+      uint32_t kk[4];
 #pragma unroll
-        for (int u = 0; u < BU; ++u) v[u] = i0 + u * kScoreThreads < np ? __ldg(bt + i0 + u * kScoreThreads) : 0;
+      for (int e = 0; e < 4; ++e) kk[e] = keys[base + 32 * e + lane];
 #pragma unroll
-        for (int u = 0; u < BU; ++u)
-          if (i0 + u * kScoreThreads < np) btrow[i0 + u * kScoreThreads] = v[u];
-      }
-      for (int s0 = tid; s0 < ncand; s0 += BU * kScoreThreads) {
-        uint2 v[BU];
-#pragma unroll
-        for (int u = 0; u < BU; ++u) {
-          const int s2 = s0 + u * kScoreThreads;
-          if (s2 < ncand) {
-            int q = 0;
-            while ((int)seg[q + 1] <= s2) ++q;
-            v[u] = __ldcg(gc + (size_t)q * p.chunk + (s2 - (int)seg[q]));
+      for (int e = 0; e < 4; ++e) {
+        const int li = base + 32 * e + lane;
+        const uint32_t d = kk[e] >> kSh1;
+        const bool in = li < w1;
+        const uint32_t mg = __ballot_sync(0xffffffffu, in && (d > D1 || (whole1 && d == D1)));
+        const bool eq = in && !whole1 && d == D1;
+        const uint32_t me = __ballot_sync(0xffffffffu, eq);
+        if (lane == 0) {
+          sh.gtm[(base >> 5) + e] = mg;
+          sh.eqm[(base >> 5) + e] = me;
+        }
+        g += __popc(mg);
+        if (me) {
+          if (eq) atomicAdd(&sh.h2[(kk[e] >> kSh2) & (kD2 - 1)], 1u);
+          if (!ovf) {
+            uint32_t slot = 0;
+            if (lane == 0) slot = atomicAdd(&sh.ncand, (uint32_t)__popc(me));
+            slot = __shfl_sync(0xffffffffu, slot, 0);
+            if (eq) sh.cand[slot + __popc(me & lt)] = make_uint2(kk[e], (uint32_t)(t0 + li));
           }
         }
-#pragma unroll
-        for (int u = 0; u < BU; ++u)
-          if (s0 + u * kScoreThreads < ncand) stage[s0 + u * kScoreThreads] = v[u];
+      }
+    }
+    if (lane == 0) sh.wcnt[warp] = g;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t s = 0;
+    for (int w = 0; w < kWarps; ++w) s += sh.wcnt[w];
+    sh.cnt[0] = s;
+    sh.cnt[1] = 0;
+  }
+  coarse_sums<32>(sh.h2, sh.c2);
+  DS_TRACE_AT(0, 3);
+
+  // iterate this CTA's keys with digit1 == D1: the list, or a full scan
+  auto for_each_cand = [&](auto &&f) {
+    if (!ovf) {
+      const int nc = (int)sh.ncand;
+      for (int i = tid; i < nc; i += kThreads) f(sh.cand[i].x, (int)sh.cand[i].y);
+    } else {
+      for (int i = tid; i < nloc; i += kThreads) {
+        const uint32_t key = keys[i];
+        if ((key >> kSh1) == D1) f(key, t0 + i);
+      }
+    }
+  };
+
+  uint32_t kB = 0;   // boundary pair: selected <=> key > kB || (key == kB && t <= tB)
+  int tB = 0x7fffffff;
+  uint32_t base_sel = 0;  // selected tokens of the lower CTAs of the cluster
+  if (whole1) {
+    kB = D1 << kSh1;  // key >= kB
+    cluster.sync();   // S2: counts
+    for (int cr = 0; cr < crank; ++cr) base_sel += cluster.map_shared_rank(sh.cnt, cr)[0];
+  } else {
+    // ---- S2: level-2 boundary -> 22-bit prefix P2
+    cluster.sync();
+    if (warp == 0) {
+      const Boundary<1> d2 = cluster_boundary<32>(cluster, nch, sh.h2, sh.c2, need1);
+      if (lane == 0) {
+        sh.state[3] = (uint32_t)d2.bin;
+        sh.state[4] = d2.above;
+        sh.state[5] = d2.cnt;
       }
     }
     __syncthreads();
-    DS_TRACE_AT(0, 3);
-    const FastScratch fs{hist, coarse, members, selbits, warp_tot, state};
-    done = select_fast<kScoreThreads>(stage, ncand, (uint32_t)keff, mm[0], mm[1], fs, idx_out, rid_out, btrow, c, h);
-    if (!done) select_core_staged<kScoreThreads>(stage, ncand, (uint32_t)keff, scr, idx_out, rid_out, c, b, h);
-  } else {
-    select_core<kScoreThreads>(GlobalSrc{gc, seg, p.chunk}, ncand, (uint32_t)keff, scr, idx_out, rid_out, c, b, h);
+    const uint32_t P2 = (D1 << (kSh1 - kSh2)) | sh.state[3];
+    const uint32_t need2 = need1 - sh.state[4];
+    const uint32_t cnt2 = sh.state[5];
+    const bool whole2 = cnt2 == need2;
+    const bool fits2 = cnt2 <= (uint32_t)kMaxMembers;
+    // members pass over the candidates: prefix > P2 are selected (>= P2 when
+    // P2 is taken whole); prefix == P2 -> member list
+    for_each_cand([&](uint32_t key, int t) {
+      const uint32_t pfx = key >> kSh2;
+      if (pfx > P2 || (whole2 && pfx == P2)) {
+        atomicAdd(&sh.cnt[1], 1u);
+      } else if (pfx == P2 && fits2) {
+        sh.members[atomicAdd(&sh.nmem, 1u)] = make_uint2(key, (uint32_t)t);
+      }
+    });
+    DS_TRACE_AT(0, 4);
+    // ---- S3: exchange members + counts
+    cluster.sync();
+    DS_TRACE_AT(0, 7);
+    for (int cr = 0; cr < crank; ++cr) {
+      const uint32_t *rc = cluster.map_shared_rank(sh.cnt, cr);
+      base_sel += rc[0] + rc[1];
+    }
+    if (whole2) {
+      kB = P2 << kSh2;
+    } else if (fits2) {
+      uint32_t off = 0;
+      for (int cr = 0; cr < nch; ++cr) {
+        const uint32_t m = cr == crank ? sh.nmem : cluster.map_shared_rank(&sh.nmem, cr)[0];
+        const uint2 *rmem = cluster.map_shared_rank(sh.members, cr);
+        for (int i = tid; i < (int)m; i += kThreads) sh.gathered[off + i] = rmem[i];
+        off += m;
+      }
+      __syncthreads();
+      const int nm = (int)cnt2;
+      for (int i = tid; i < nm; i += kThreads) {
+        const uint2 me = sh.gathered[i];
+        uint32_t rank = 0;
+        for (int j = 0; j < nm; ++j) {
+          const uint2 o = sh.gathered[j];
+          rank += (o.x > me.x) || (o.x == me.x && o.y < me.y);
+        }
+        if (rank == need2 - 1) {
+          sh.state[6] = me.x;
+          sh.state[7] = me.y;
+        }
+        if (rank < need2 && (int)me.y < t0) atomicAdd(&sh.lower_sel, 1u);
+      }
+      __syncthreads();
+      kB = sh.state[6];
+      tB = (int)sh.state[7];
+      base_sel += sh.lower_sel;
+    } else {
+      // ---- massive ties at P2: level-3 digit (bits 9..0) over the cluster,
+      // then the token order among keys equal to kB
+      uint32_t *h3 = sh.h1;  // h1 / c1 are no longer read by any CTA (after S2)
+      uint32_t *c3 = sh.c1;
+      for (int i = tid; i < kD3; i += kThreads) h3[i] = 0;
+      __syncthreads();
+      for_each_cand([&](uint32_t key, int t) {
+        if ((key >> kSh2) == P2) atomicAdd(&h3[key & (kD3 - 1)], 1u);
+      });
+      __syncthreads();
+      coarse_sums<32>(h3, c3);
+      cluster.sync();
+      if (warp == 0) {
+        const Boundary<1> d3 = cluster_boundary<32>(cluster, nch, h3, c3, need2);
+        if (lane == 0) {
+          sh.state[6] = (uint32_t)d3.bin;
+          sh.state[7] = d3.above;
+        }
+      }
+      __syncthreads();
+      const uint32_t D3 = sh.state[6];
+      kB = (P2 << kSh2) | D3;
+      const uint32_t rem = need2 - sh.state[7];  // keys == kB to take, in token order
+      uint32_t eq_lower = 0;
+      for (int cr = 0; cr < crank; ++cr) eq_lower += cluster.map_shared_rank(h3, cr)[D3];
+      const uint32_t my_eq = h3[D3];
+      const uint32_t take = rem > eq_lower ? min(rem - eq_lower, my_eq) : 0u;
+      // tB = my take-th key equal to kB in token order (none: -1, all: max)
+      if (take == 0) {
+        tB = -1;
+      } else if (take == my_eq) {
+        tB = 0x7fffffff;
+      } else {
+        uint32_t e = 0;  // per-warp counts of keys == kB
+        for (int base = w0; base < w1; base += 32)
+          e += __popc(__ballot_sync(0xffffffffu, base + lane < w1 && keys[base + lane] == kB));
+        __syncthreads();
+        if (lane == 0) sh.wcnt[warp] = e;
+        __syncthreads();
+        uint32_t before = 0;
+        for (int w = 0; w < warp; ++w) before += sh.wcnt[w];
+        if (before < take && before + e >= take) {  // this warp holds the take-th one
+          uint32_t run = before;
+          for (int base = w0; base < w1; base += 32) {
+            const bool q = base + lane < w1 && keys[base + lane] == kB;
+            const uint32_t m = __ballot_sync(0xffffffffu, q);
+            if (run + __popc(m) >= take) {
+              const int sel = __fns(m, 0, (int)(take - run));
+              if (lane == 0) sh.state[5] = (uint32_t)(t0 + base + sel);
+              break;
+            }
+            run += __popc(m);
+          }
+        }
+        __syncthreads();
+        tB = (int)sh.state[5];
+      }
+      // per-warp selected counts and the CTA total, exchanged once more
+      uint32_t g = 0;
+      for (int base = w0; base < w1; base += 32) {
+        const int li = base + lane;
+        const uint32_t key = li < w1 ? keys[li] : 0u;
+        g += __popc(__ballot_sync(0xffffffffu, li < w1 && (key > kB || (key == kB && t0 + li <= tB))));
+      }
+      __syncthreads();
+      if (lane == 0) sh.wcnt[warp] = g;
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t s = 0;
+        for (int w = 0; w < kWarps; ++w) s += sh.wcnt[w];
+        sh.cnt[3] = s;
+      }
+      cluster.sync();
+      base_sel = 0;
+      for (int cr = 0; cr < crank; ++cr) base_sel += cluster.map_shared_rank(sh.cnt, cr)[3];
+    }
   }
-  DS_TRACE_AT(0, 4);
-  // ---- publish
-  __syncthreads();
-  if (tid == 0) {
-    p.counter[unit] = 0u;
+  DS_TRACE_AT(0, 8);
+
+  // ---- ordered write of the selected tokens (ascending) + their row ids:
+  // lane l of warp w owns the l-th 32-token group of the warp's range
+  {
+    const int ng = (w1 - w0 + 31) >> 5;  // <= 32 groups per warp
+    const int grp = (w0 >> 5) + lane;
+    uint32_t sel = 0;
+    if (lane < ng) {
+      sel = sh.gtm[grp];
+      uint32_t e = sh.eqm[grp];
+      while (e) {
+        const int bit = __ffs(e) - 1;
+        e &= e - 1;
+        const uint32_t key = keys[grp * 32 + bit];
+        if (key > kB || (key == kB && t0 + grp * 32 + bit <= tB)) sel |= 1u << bit;
+      }
+    }
+    const uint32_t cntl = __popc(sel);
+    uint32_t incl = cntl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    __syncthreads();  // wcnt is scratch of the passes above
+    if (lane == 31) sh.wcnt[warp] = incl;
+    __syncthreads();
+    uint32_t pos = base_sel + incl - cntl;
+    for (int w = 0; w < warp; ++w) pos += sh.wcnt[w];
+    DS_TRACE_AT(0, 10);
+    while (sel) {
+      const int bit = __ffs(sel) - 1;
+      sel &= sel - 1;
+      const int t = t0 + grp * 32 + bit;
+      idx_out[pos] = t;
+      rid_out[pos] = rowid_of(t);
+      ++pos;
+    }
+  }
+  DS_TRACE_AT(0, 5);
+  // ---- S4: exit guard (DSMEM lifetime) + every CTA's writes done; publish
+  cluster.sync();
+  if (crank == 0 && tid == 0) {
     __threadfence();
     atomicExch(p.ready + unit, 1u);
   }
+  DS_TRACE_AT(0, 6);
 }
 
 // ------------------------------------------------------------- launch
 template <typename T, int R>
-static cudaError_t launch_score_t(const ScoreParams &p, int units, int nchunks, size_t smem, cudaStream_t st) {
-  static const cudaError_t attr = cudaFuncSetAttribute(score_select_kernel<T, R>,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+static cudaError_t launch_score_t(const ScoreParams &p, int units, int nch, size_t smem, cudaStream_t st) {
+  static const cudaError_t attr = [] {
+    cudaError_t e = cudaFuncSetAttribute(score_select_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kMaxDynSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(score_select_kernel<T, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return e;
+  }();
   if (attr != cudaSuccess) return attr;
-  return PdlLaunch(dim3(nchunks, units), dim3(kScoreThreads), smem, st).run(score_select_kernel<T, R>, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nch, units);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute a[2];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = nch;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, score_select_kernel<T, R>, p);
 }
 
-SelectGeom select_geom(const ds_cache *c, int k) {
+SelectGeom select_geom(const ds_cache *c) {
   SelectGeom g{};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int units = c->batch * c->num_kv_heads;
-  // CTAs per unit: enough for one wave at 2 CTAs/SM, but chunks of >= 4k
-  // tokens so that each chunk's local top-k superset stays small (~k); each
-  // chunk's keys fit in shared memory
-  const int per_sm = 2;
-  int nch = (per_sm * sms) / units;
-  const int kk = k < 1 ? 1 : k;
-  const int by_k = c->max_seq_len / (4 * kk);
-  if (nch > by_k) nch = by_k;
+  // cluster size: as many CTAs per unit as fill the GPU at 2 CTAs/SM (<= 8,
+  // portable), more only if a chunk's keys would not fit in shared memory
+  int nch = (2 * sms) / units;
+  if (nch > 8) nch = 8;
   const int need = (c->max_seq_len + kMaxChunkLen - 1) / kMaxChunkLen;
   if (nch < need) nch = need;
-  nch = nch < 1 ? 1 : (nch > kMaxChunks ? kMaxChunks : nch);
+  if (nch < 1) nch = 1;
+  if (nch > kMaxChunks) nch = kMaxChunks;
   int chunk = (c->max_seq_len + nch - 1) / nch;
   chunk = (chunk + 255) & ~255;
   g.chunk = chunk;
   g.nchunks = (c->max_seq_len + chunk - 1) / chunk;
-  // dynamic smem holds the chunk's keys, then the unit's staged candidates
-  // (expected ~nchunks * (k + a bin); the global path covers overflow)
-  size_t stage = (size_t)g.nchunks * (kk + kk / 2) + 64;
-  // the stage, the block-table row and the bitmap must fit kMaxDynSmem
-  const size_t fixed = (size_t)c->max_pages_per_seq * 4 + 4096 + 1024;
-  const size_t cap_max = (kMaxDynSmem - fixed) / (8 + 1);
-  if (stage > cap_max) stage = cap_max;
-  size_t bytes = (size_t)chunk * 4;
-  if (stage * 8 > bytes) bytes = stage * 8;
-  bytes += 1024;  // 128-bit loads run up to 127 keys / candidates past the end
-  g.stage_cap = (int)(bytes / 8);
-  // after the stage: the block-table row and the selected-members bitmap
-  bytes += (size_t)c->max_pages_per_seq * 4 + ((size_t)g.stage_cap / 32 + 1) * 4;
-  g.score_smem = (bytes + 15) & ~(size_t)15;
-  g.threads = kScoreThreads;
+  // keys [chunk] + 128 pad + this chunk's block-table entries (if few enough)
+  const int pages = chunk / c->page_size + 2;
+  g.score_smem = ((size_t)chunk + 128) * 4 + (pages <= kMaxPageRow ? (size_t)pages * 4 : 0);
+  g.score_smem = (g.score_smem + 15) & ~(size_t)15;
+  g.threads = kThreads;
   return g;
 }
 
-size_t select_workspace_cand(const ds_cache *c) {
-  return (size_t)c->batch * c->num_kv_heads * cand_stride(c->max_seq_len) * 8;
-}
-size_t select_workspace_count(const ds_cache *c) { return (size_t)c->batch * c->num_kv_heads * kMaxChunks * 4; }
-
 cudaError_t launch_score(const ds_cache *c, const ScoreParams &p, const SelectGeom &g, cudaStream_t st) {
   const int units = c->batch * c->num_kv_heads;
-  if (g.chunk > kMaxChunkLen) return cudaErrorInvalidValue;
+  if (g.chunk > kMaxChunkLen || g.nchunks > kMaxChunks || g.score_smem > (size_t)kMaxDynSmem)
+    return cudaErrorInvalidValue;
 #define DS_SCORE(T, R) launch_score_t<T, R>(p, units, g.nchunks, g.score_smem, st)
   switch (c->dtype) {
     case DS_BF16:

@@ -39,6 +39,16 @@ for it in range(4):
 L.ds_debug_read_trace(buf.ctypes.data_as(ctypes.c_void_p), buf.nbytes)
 
 
+def report_slots(kind, pairs):
+    t = buf[kind].astype(np.int64)
+    t = t[t[:, 0] > 0]
+    for a, b_, nm in pairs:
+        ok = (t[:, a] > 0) & (t[:, b_] > 0)
+        if ok.any():
+            d = (t[ok, b_] - t[ok, a]) / 1e3
+            print(f"  sub {nm:14s} p50 {np.median(d):7.2f} p90 {np.percentile(d, 90):7.2f}")
+
+
 def report(kind, names):
     t = buf[kind].astype(np.int64)
     t = t[t[:, 0] > 0]
@@ -60,7 +70,11 @@ def report(kind, names):
             print(f"  dur {names[i - 1]}->{names[i]:14s} p50 {np.median(d):7.2f} p90 {np.percentile(d, 90):7.2f} max {d.max():7.2f}")
 
 
-report(0, ["start", "streamed", "emitted", "staged", "selected"])
+report(0, ["start", "streamed", "S1 D1", "L2 pass", "members", "written", "published"])
+report_slots(0, [(4, 7, "S3 sync"), (7, 8, "gather+rank"), (8, 10, "pre-write"), (10, 5, "write pass")])
+_bc = buf[0][:, 9][buf[0][:, 0] > 0]
+if len(_bc):
+    print("  boundary-bin members p50", np.median(_bc), "p90", np.percentile(_bc, 90), "max", _bc.max())
 
 
 def report1():
