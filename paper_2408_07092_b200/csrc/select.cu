@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, 2) score_select_kernel(ScoreParams p
     keys[i] = k0;
     atomicAdd(&sh.h1[k0 >> kSh1], 1u);
   }
+  if (tid < 128) keys[nloc + tid] = 0u;  // pad: below every finite score's key
   DS_TRACE_AT(0, 1);
 
   const bool pow2 = (c.P & (c.P - 1)) == 0;
@@ -319,10 +320,14 @@ __global__ void __launch_bounds__(kThreads, 2) score_select_kernel(ScoreParams p
   DS_TRACE_AT(0, 2);
 
   // ---- L2: per 32-token group, ballot masks of digit1 > D1 (>= D1 when D1
-  // is taken whole) and digit1 == D1; the D1 keys (a few hundred) go to the
-  // candidate list and the level-2 histogram
+  // is taken whole) and digit1 == D1 (keys past nloc are 0: below any
+  // finite score's key)
   const uint32_t lt = lanemask_lt();
+  const int ng = (w1 - w0 + 31) >> 5;  // this warp's groups (<= 32)
+  const int grp = (w0 >> 5) + lane;    // lane-per-group passes: my group
   {
+    const int gcmp = whole1 ? (int)D1 - 1 : (int)D1;
+    const uint32_t ecmp = whole1 ? 0xffffffffu : D1;
     uint32_t g = 0;
     for (int base = w0; base < w1; base += 128) {
       uint32_t kk[4];
@@ -330,29 +335,39 @@ __global__ void __launch_bounds__(kThreads, 2) score_select_kernel(ScoreParams p
       for (int e = 0; e < 4; ++e) kk[e] = keys[base + 32 * e + lane];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int li = base + 32 * e + lane;
         const uint32_t d = kk[e] >> kSh1;
-        const bool in = li < w1;
-        const uint32_t mg = __ballot_sync(0xffffffffu, in && (d > D1 || (whole1 && d == D1)));
-        const bool eq = in && !whole1 && d == D1;
-        const uint32_t me = __ballot_sync(0xffffffffu, eq);
-        if (lane == 0) {
+        const uint32_t mg = __ballot_sync(0xffffffffu, (int)d > gcmp);
+        const uint32_t me = __ballot_sync(0xffffffffu, d == ecmp);
+        if (lane == e) {
           sh.gtm[(base >> 5) + e] = mg;
           sh.eqm[(base >> 5) + e] = me;
         }
         g += __popc(mg);
-        if (me) {
-          if (eq) atomicAdd(&sh.h2[(kk[e] >> kSh2) & (kD2 - 1)], 1u);
-          if (!ovf) {
-            uint32_t slot = 0;
-            if (lane == 0) slot = atomicAdd(&sh.ncand, (uint32_t)__popc(me));
-            slot = __shfl_sync(0xffffffffu, slot, 0);
-            if (eq) sh.cand[slot + __popc(me & lt)] = make_uint2(kk[e], (uint32_t)(t0 + li));
-          }
-        }
       }
     }
     if (lane == 0) sh.wcnt[warp] = g;
+    __syncwarp();
+    // the D1 keys (a few hundred): candidate list + level-2 histogram
+    if (!whole1) {
+      uint32_t e = lane < ng ? sh.eqm[grp] : 0u;
+      const uint32_t ne = __popc(e);
+      uint32_t incl = ne;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      uint32_t slot = 0;
+      if (lane == 31 && incl && !ovf) slot = atomicAdd(&sh.ncand, incl);
+      slot = __shfl_sync(0xffffffffu, slot, 31) + incl - ne;
+      while (e) {
+        const int bit = __ffs(e) - 1;
+        e &= e - 1;
+        const uint32_t key = keys[grp * 32 + bit];
+        atomicAdd(&sh.h2[(key >> kSh2) & (kD2 - 1)], 1u);
+        if (!ovf) sh.cand[slot++] = make_uint2(key, (uint32_t)(t0 + grp * 32 + bit));
+      }
+    }
   }
   __syncthreads();
   if (tid == 0) {
@@ -531,8 +546,6 @@ __global__ void __launch_bounds__(kThreads, 2) score_select_kernel(ScoreParams p
   // ---- ordered write of the selected tokens (ascending) + their row ids:
   // lane l of warp w owns the l-th 32-token group of the warp's range
   {
-    const int ng = (w1 - w0 + 31) >> 5;  // <= 32 groups per warp
-    const int grp = (w0 >> 5) + lane;
     uint32_t sel = 0;
     if (lane < ng) {
       sel = sh.gtm[grp];

@@ -27,3 +27,12 @@ runs.sort(key=lambda x: -(x[1] * x[2]))
 for s, c, n, smp in runs[: int(sys.argv[2]) if len(sys.argv) > 2 else 25]:
     print(f"idx {s:5d} n={n:4d} exec={c:8d} total={c * n:10d} ({100 * c * n / tot:5.1f}%) samples={smp:6d} "
           f"({100 * smp / max(stot, 1):4.1f}%)  {data[s][src].strip()[:50]}")
+
+if len(sys.argv) > 3:  # region stall breakdown: sass_hot.py CSV N a:b,c:d,...
+    cols = [i for i, n in enumerate(h) if n.startswith("stall_")]
+    for reg in sys.argv[3].split(","):
+        a, b = map(int, reg.split(":"))
+        tot_s = {h[i]: sum(int(r[i] or 0) for r in data[a:b]) for i in cols}
+        ssum = sum(int(r[sm] or 0) for r in data[a:b])
+        top = sorted(tot_s.items(), key=lambda x: -x[1])[:6]
+        print(f"[{a}:{b}] samples {ssum} ({100 * ssum / max(stot, 1):.1f}%):", ", ".join(f"{k[6:]}={v}" for k, v in top))
