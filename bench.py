@@ -39,7 +39,8 @@ from paper_2408_07092_b200 import ledger  # noqa: E402
 
 METRIC = "sparse decode-attn µs/layer & HBM GB/s vs dense, S=32K, 1/16 sparsity, 1-8 B200"
 KERNELS_PER_APPEND = 1
-KERNELS_PER_DECODE = 2      # score+select (cluster per unit), split-K attention (cluster per unit)
+# kernels per ds_decode_attention call: ds_decode_launches() (1 = fused decode_kernel,
+# 2 = cluster score_select_kernel + attention kernel)
 KERNELS_PER_DENSE = 1
 
 
@@ -271,6 +272,7 @@ def run_ours(args, dist):
         "bytes_alg_per_layer": bytes_layer,
     }
     achieved = bytes_layer / (us_decode * 1e-6) / 1e9
+    n_dec = ds.ds_decode_launches(layers[0]["cache"], cfg.k)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{full.name}.json")
     if os.path.exists(tpath):
@@ -280,10 +282,11 @@ def run_ours(args, dist):
             traffic = None
     res["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                        "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-                       "kernel": "ds_decode_attention launch group (score_select_kernel + attn_kernel)",
+                       "kernel": ("decode_kernel (fused score+select+attention, one CTA per unit)" if n_dec == 1 else
+                                  "ds_decode_attention launch group (score_select_kernel + attn_mma_kernel)"),
                        "us_per_launch": round(us_decode, 3), "peak_source": peak_src,
                        "algorithmic_bytes_per_launch": bytes_layer}
-    res["gpu_launches"] = args.steps * L * (KERNELS_PER_APPEND + KERNELS_PER_DECODE)
+    res["gpu_launches"] = args.steps * L * (KERNELS_PER_APPEND + n_dec)
     if clocks:
         res["clocks"] = clocks
 

@@ -144,6 +144,14 @@ ds_status ds_decode_attention(const ds_cache *c, const void *q, int32_t k, void 
                               int32_t *topk_idx_out, void *workspace, size_t workspace_bytes,
                               cudaStream_t stream);
 
+/* Number of kernels one ds_decode_attention call with this cache and k
+ * enqueues (0 on invalid arguments): 1 when the whole of Algorithm 1 runs
+ * as one kernel with one CTA per (b, KV head) unit (16-bit KV, max_seq_len
+ * <= 32768, enough units to cover the GPU), else 2 (score+select with the
+ * CTAs of a unit in one thread-block cluster, then the attention).  Results
+ * are identical up to the fp32 summation order of the attention. */
+int32_t ds_decode_launches(const ds_cache *c, int32_t k);
+
 /* Lines 1-2 of Algorithm 1 only, for diagnostics and tests:
  * scores_out fp32 [batch][num_kv_heads][max_seq_len]; entries t >=
  * seq_lens[b] are left untouched.  Same arithmetic as ds_decode_attention. */

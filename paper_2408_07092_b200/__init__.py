@@ -69,6 +69,8 @@ def lib():
         L.ds_decode_workspace_size.restype = SZ
         L.ds_decode_attention.argtypes = [C, P, I32, P, P, P, SZ, P]
         L.ds_approx_scores.argtypes = [C, P, P, P]
+        L.ds_decode_launches.argtypes = [C, I32]
+        L.ds_decode_launches.restype = I32
         L.ds_dense_workspace_size.argtypes = [C]
         L.ds_dense_workspace_size.restype = SZ
         L.ds_dense_decode_attention.argtypes = [C, P, P, P, SZ, P]
@@ -81,7 +83,7 @@ def lib():
 
 EXPORTS = ("ds_status_string", "ds_version", "ds_calibrate_channels", "ds_append_kv",
            "ds_decode_workspace_size", "ds_decode_attention", "ds_approx_scores",
-           "ds_dense_workspace_size", "ds_dense_decode_attention")
+           "ds_dense_workspace_size", "ds_dense_decode_attention", "ds_decode_launches")
 
 
 def ds_status_string(s: int) -> str:
@@ -179,6 +181,11 @@ def ds_append_kv(cache: LayerCache, k_new, v_new, positions, stream=None, cs=Non
 
 def ds_decode_workspace_size(cache: LayerCache, k: int) -> int:
     return lib().ds_decode_workspace_size(ctypes.byref(cache.struct()), k)
+
+
+def ds_decode_launches(cache: LayerCache, k: int) -> int:
+    """Kernels one ds_decode_attention call enqueues: 1 (fused) or 2."""
+    return lib().ds_decode_launches(ctypes.byref(cache.struct()), k)
 
 
 def ds_dense_workspace_size(cache: LayerCache) -> int:

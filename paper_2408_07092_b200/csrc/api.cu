@@ -126,6 +126,11 @@ size_t ds_decode_workspace_size(const ds_cache *c, int32_t k) {
   return carve_workspace(c, k, nullptr).bytes;
 }
 
+int32_t ds_decode_launches(const ds_cache *c, int32_t k) {
+  if (validate_cache(c) != DS_OK || k < 1 || k > c->max_seq_len) return 0;
+  return fused_applicable(c) ? 1 : 2;
+}
+
 static void fill_attn(AttnParams &ap, const ds_cache *c, const void *q, const int32_t *rowid, int k,
                       const AttnGeom &ag, void *out) {
   ap.c = make_view(c);
@@ -145,6 +150,16 @@ ds_status ds_decode_attention(const ds_cache *c, const void *q, int32_t k, void 
   if (k < 1 || k > c->max_seq_len || !q || !out || !aligned16(q) || !aligned16(out)) return DS_ERR_INVALID_ARGUMENT;
   Workspace w = carve_workspace(c, k, workspace);
   if (!workspace || workspace_bytes < w.bytes || !aligned16(workspace)) return DS_ERR_WORKSPACE_TOO_SMALL;
+  if (fused_applicable(c)) {  // serving shape: one kernel, one CTA per unit
+    FusedParams fp;
+    fp.c = make_view(c);
+    fp.q = q;
+    fp.k = k;
+    fp.out = out;
+    fp.idx = topk_idx_out;
+    fp.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c->head_dim));
+    return cuda_status(launch_fused(c, fp, stream));
+  }
   SelectGeom sg = select_geom(c);
   AttnGeom ag = attn_geom(c, k);
   if (ag.nsplit < 1) return DS_ERR_UNSUPPORTED;

@@ -76,6 +76,25 @@ template <> struct Mma<__half> {
   }
 };
 
+// m16n8k8: A 16x8 (a0 rows 0-7, a1 rows 8-15), B 8x8 (one register)
+template <typename T> struct Mma8;
+template <> struct Mma8<__nv_bfloat16> {
+  __device__ static __forceinline__ void run(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(b0));
+  }
+};
+template <> struct Mma8<__half> {
+  __device__ static __forceinline__ void run(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(b0));
+  }
+};
+
 __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2,
                                                   uint32_t &r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
@@ -168,6 +187,58 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// --------------------------------------------------- histogram boundary
+// One warp: boundary of a histogram held NPL bins per lane, bins in
+// descending order hi_bin - NPL*lane - j.  With `base` keys above the
+// first bin and `need` wanted from the top, returns the bin d with
+// above(d) < need <= above(d) + cnt(d).
+template <int NPL>
+struct Boundary {
+  int bin;
+  uint32_t above, cnt;
+};
+template <int NPL>
+__device__ __forceinline__ Boundary<NPL> warp_boundary(const uint32_t (&v)[NPL], int hi_bin, uint32_t base,
+                                                       uint32_t need) {
+  const int lane = threadIdx.x & 31;
+  uint32_t tot = 0;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) tot += v[j];
+  uint32_t incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  uint32_t run = base + incl - tot;
+  int hit = -1;
+  uint32_t ha = 0, hc = 0;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    if (hit < 0 && run < need && run + v[j] >= need) {
+      hit = j;
+      ha = run;
+      hc = v[j];
+    }
+    run += v[j];
+  }
+  const uint32_t m = __ballot_sync(0xffffffffu, hit >= 0);
+  const int src = m ? __ffs(m) - 1 : 31;
+  Boundary<NPL> r;
+  r.bin = hi_bin - NPL * src - __shfl_sync(0xffffffffu, hit < 0 ? 0 : hit, src);
+  r.above = __shfl_sync(0xffffffffu, ha, src);
+  r.cnt = __shfl_sync(0xffffffffu, hc, src);
+  return r;
+}
+
+// named barriers (id 0 is __syncthreads)
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 }  // namespace ds
 
 // ------------------------------------------------------------ tracing
@@ -179,10 +250,11 @@ namespace ds {
 constexpr int kTraceCtas = 4096, kTraceSlots = 16;
 __device__ unsigned long long g_trace[3][kTraceCtas][kTraceSlots];  // unity trace build: one TU
 }
-#define DS_TRACE_AT(kind, slot)                                                              \
+#define DS_TRACE_AT(kind, slot) DS_TRACE_BY(kind, slot, 0)
+#define DS_TRACE_BY(kind, slot, thread)                                                      \
   do {                                                                                       \
     const unsigned cta_ = blockIdx.x + blockIdx.y * gridDim.x;                              \
-    if (threadIdx.x == 0 && cta_ < (unsigned)ds::kTraceCtas) {                               \
+    if (threadIdx.x == (thread) && cta_ < (unsigned)ds::kTraceCtas) {                        \
       unsigned long long t_;                                                                 \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                \
       ds::g_trace[kind][cta_][slot] = t_;                                                    \
@@ -191,5 +263,8 @@ __device__ unsigned long long g_trace[3][kTraceCtas][kTraceSlots];  // unity tra
 #else
 #define DS_TRACE_AT(kind, slot) \
   do {                          \
+  } while (0)
+#define DS_TRACE_BY(kind, slot, thread) \
+  do {                                  \
   } while (0)
 #endif

@@ -39,6 +39,19 @@ struct AttnParams {
   void *out;                // [B][Hq][D]
 };
 
+// decode_kernel (decode.cu): the whole of Algorithm 1 per unit in one CTA.
+struct FusedParams {
+  CacheView c;
+  const void *q;     // [B][Hq][D]
+  int k;
+  void *out;         // [B][Hq][D]
+  int32_t *idx;      // nullable [units][k]
+  float scale_log2;  // log2(e) / sqrt(D)
+};
+constexpr int kFusedMaxSmem = 227 * 1024;
+bool fused_applicable(const ds_cache *c);
+cudaError_t launch_fused(const ds_cache *c, const FusedParams &p, cudaStream_t st);
+
 // Launch-geometry decisions (deterministic functions of the cache shape).
 struct SelectGeom {
   int chunk, nchunks;  // score CTAs per unit (one cluster)

@@ -86,49 +86,6 @@ struct SelSh {
   uint32_t ncand, nmem, lower_sel, pad;
 };
 
-// Warp 0: boundary of a histogram held NPL bins per lane, bins in
-// descending order hi_bin - NPL*lane - j.  With `base` keys above the
-// first bin and `need` wanted from the top, returns the bin d with
-// above(d) < need <= above(d) + cnt(d).
-template <int NPL>
-struct Boundary {
-  int bin;
-  uint32_t above, cnt;
-};
-template <int NPL>
-__device__ __forceinline__ Boundary<NPL> warp_boundary(const uint32_t (&v)[NPL], int hi_bin, uint32_t base,
-                                                       uint32_t need) {
-  const int lane = threadIdx.x & 31;
-  uint32_t tot = 0;
-#pragma unroll
-  for (int j = 0; j < NPL; ++j) tot += v[j];
-  uint32_t incl = tot;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  uint32_t run = base + incl - tot;
-  int hit = -1;
-  uint32_t ha = 0, hc = 0;
-#pragma unroll
-  for (int j = 0; j < NPL; ++j) {
-    if (hit < 0 && run < need && run + v[j] >= need) {
-      hit = j;
-      ha = run;
-      hc = v[j];
-    }
-    run += v[j];
-  }
-  const uint32_t m = __ballot_sync(0xffffffffu, hit >= 0);
-  const int src = m ? __ffs(m) - 1 : 31;
-  Boundary<NPL> r;
-  r.bin = hi_bin - NPL * src - __shfl_sync(0xffffffffu, hit < 0 ? 0 : hit, src);
-  r.above = __shfl_sync(0xffffffffu, ha, src);
-  r.cnt = __shfl_sync(0xffffffffu, hc, src);
-  return r;
-}
-
 // Cluster-wide boundary over a histogram of 64*64 (NC=64, coarse sums in c)
 // or 32*32 (NC=32) bins, each CTA holding its own copy; warp 0 only.
 template <int NC>

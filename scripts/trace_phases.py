@@ -56,7 +56,7 @@ def report(kind, names):
         print("no trace for kind", kind)
         return
     t0 = min(buf[k][buf[k][:, 0] > 0][:, 0].min() for k in range(3) if (buf[k][:, 0] > 0).any())
-    print(f"\n{['score_select', 'select', 'attention'][kind]}: {len(t)} CTAs")
+    print(f"\n{['score_select', 'fused decode', 'attention'][kind]}: {len(t)} CTAs")
     for i, n in enumerate(names):
         ok = t[:, i] > 0
         if not ok.any():
@@ -94,3 +94,4 @@ def report1():
         if ok.any():
             prev = s_
 report(2, ["start", "rowids", "loop done", "cluster sync", "merged"])
+report(1, ["start", "streamed", "masks", "tail done", "gt rows done", "all rows", "merged"])

@@ -72,6 +72,9 @@ def check_units(lay, cache, C, k, units, y_gpu, idx_gpu):
     for b, h in units:
         q, K, V = unit_host(lay, b, h)
         S = K.shape[0]
+        if S == 0:  # empty sequence: nothing selected, y = 0 (ds.h)
+            assert np.all(idx_gpu[b, h] == -1) and np.all(y_gpu[b, h * G:(h + 1) * G] == 0)
+            continue
         L = oracle.label_gather(K, Ch[h])
         y_ref, idx_ref, shat, tau = oracle.ds_decode_unit(q, K, V, L, Ch[h], k)
         keff = min(k, S)
