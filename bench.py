@@ -35,7 +35,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import synth  # noqa: E402
-from paper_2408_07092_b200 import ledger  # noqa: E402
+from paper_2408_07092_b200 import ledger, shard  # noqa: E402
 
 METRIC = "sparse decode-attn µs/layer & HBM GB/s vs dense, S=32K, 1/16 sparsity, 1-8 B200"
 KERNELS_PER_APPEND = 1
@@ -110,29 +110,70 @@ def shard_plan(cfg: synth.Config, world: int, rank: int, mode: str):
     allgather: a contiguous slice of KV heads (and their G query heads)."""
     if mode == "weak" or world == 1:
         return cfg, 0
-    if cfg.Hkv % world != 0:
-        raise SystemExit(f"--mode allgather needs H_kv ({cfg.Hkv}) divisible by {world}")
-    hk = cfg.Hkv // world
-    return cfg.with_(Hkv=hk, Hq=cfg.G * hk), rank * hk
+    try:
+        h0, h1 = shard.kv_head_slice(cfg.Hkv, world, rank)
+    except ValueError as e:
+        raise SystemExit(f"--mode allgather: {e}")
+    return cfg.with_(Hkv=h1 - h0, Hq=cfg.G * (h1 - h0)), h0
 
 
 # ------------------------------------------------------------------ clocks
 class Clocks:
+    """SM clock / throttle-reason sampler (NVML, every ~2 ms) running across the
+    timed region; falls back to `nvidia-smi -lms 100` without pynvml."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
     def __init__(self, gpu_index: int, path: str):
-        self.path = path
-        self.proc = None
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        import threading
+        self.rows, self.path, self.proc, self.nv = [], path, None, None
         try:
-            self.f = open(path, "w")
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+            self.stop_ev = threading.Event()
+            self.th = threading.Thread(target=self._loop, daemon=True)
+            self.th.start()
         except Exception:
-            self.proc = None
+            self.nv = None
+            q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            try:
+                self.f = open(path, "w")
+                self.proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}",
+                                              "--format=csv,noheader,nounits", "-lms", "100"],
+                                             stdout=self.f, stderr=subprocess.DEVNULL)
+            except Exception:
+                self.proc = None
+
+    def _loop(self):
+        nv, h = self.nv, self.h
+        while not self.stop_ev.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                self.rows.append((float(sm), int(rs), pw))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def stop(self):
+        if self.nv is not None:
+            self.stop_ev.set()
+            self.th.join(timeout=2)
+            if not self.rows:
+                return None
+            with open(self.path, "w") as f:
+                f.write("sm_mhz,reasons_mask,power_w\n")
+                for r in self.rows:
+                    f.write(f"{r[0]},{r[1]:#x},{r[2]}\n")
+            reasons = sorted({n for r in self.rows for bit, n in self.REASONS.items() if r[1] & bit})
+            return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": self.max_mhz,
+                    "reasons": reasons, "samples": len(self.rows), "power_w_max": max(r[2] for r in self.rows),
+                    "source": "nvml, 2 ms"}
         if not self.proc:
             return None
         self.proc.terminate()
@@ -152,8 +193,7 @@ class Clocks:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for p in rows for i in range(4) if p[5 + i].strip() == "Active"})
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
-                "samples": len(rows), "power_w_max": max(float(p[3]) for p in rows if p[3].replace(".", "").isdigit())
-                if any(p[3].replace(".", "").isdigit() for p in rows) else None}
+                "samples": len(rows), "source": "nvidia-smi, 100 ms"}
 
 
 # ----------------------------------------------------------- our GPU arm
@@ -181,9 +221,11 @@ def build_layers(cfg, L, rank, structure, device):
     return layers
 
 
-def time_graph(fn, steps, warmup, dist, stream):
+def time_graph(fn, steps, warmup, dist, stream, sampler=None):
     """Capture fn() in a CUDA graph, replay W times, then time exactly K replays
-    with events on the capture stream (barrier + sync on both sides)."""
+    with events on the capture stream (barrier + sync on both sides).
+    sampler(): started right before the timed replays, stopped right after;
+    its result is returned as a third value."""
     with torch.cuda.stream(stream):
         fn()                                   # eager warm-up (attribute setup, allocator)
     torch.cuda.synchronize()
@@ -196,13 +238,17 @@ def time_graph(fn, steps, warmup, dist, stream):
         torch.cuda.synchronize()
         dist.barrier()
         torch.cuda.synchronize()
+        smp = sampler() if sampler else None
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(steps):
             g.replay()
         e1.record(stream)
         torch.cuda.synchronize()
+        sampled = smp.stop() if smp else None
     dist.barrier()
+    if sampler:
+        return e0.elapsed_time(e1), g, sampled
     return e0.elapsed_time(e1), g
 
 
@@ -234,17 +280,17 @@ def run_ours(args, dist):
                                               P(ly["out"].data_ptr()), None, P(ws.data_ptr()), ws.numel(), sp),
                       "decode")
             if gathered is not None:
-                dist.pg.all_gather_into_tensor(gathered[i], ly["out"])
+                shard.allgather_heads(dist.pg, ly["out"], gathered[i])   # the path's one exchange step
 
     def decode_only():
         for ly in layers:
             lib.ds_decode_attention(ctypes.byref(ly["cs"]), P(ly["q"].data_ptr()), k, P(ly["out"].data_ptr()), None,
                                     P(ws.data_ptr()), ws.numel(), sp)
 
-    clk = Clocks(dist.local, os.path.join(ROOT, "gpurun_out", f"clocks_rank{dist.rank}.csv")) \
-        if dist.rank == 0 else None
-    ms_total, _ = time_graph(step, args.steps, args.warmup, dist, stream)
-    clocks = clk.stop() if clk else None
+    cpath = os.path.join(ROOT, "gpurun_out", f"clocks_rank{dist.rank}.csv")
+    os.makedirs(os.path.dirname(cpath), exist_ok=True)
+    ms_total, _, clocks = time_graph(step, args.steps, args.warmup, dist, stream,
+                                     sampler=lambda: Clocks(dist.local, cpath))
     ms_step = dist.max(ms_total / args.steps)
 
     # dominant launch group for the roofline: ds_decode_attention alone over the same layers
@@ -421,7 +467,9 @@ def cpu_baseline(cfg: synth.Config, budget_s: float = 12.0, nthreads=None):
     time budget (pilot-timed)."""
     import oracle
     nthreads = nthreads or os.cpu_count() or 1
-    sc, q, K, V, L, C, sl = oracle_sample(cfg, 1, seed=cfg.seed_base + 777)
+    n_seq = max(1, -(-nthreads // cfg.Hkv))            # enough units to occupy every core
+    sc, q, K, V, L, C, sl = oracle_sample(cfg, n_seq, seed=cfg.seed_base + 777)
+    nthreads = min(nthreads, sc.units)
     t = time.perf_counter()
     oracle.decode_batch(q, K, V, L, C, sl, cfg.k, nthreads=nthreads)
     pilot = time.perf_counter() - t
@@ -433,7 +481,7 @@ def cpu_baseline(cfg: synth.Config, budget_s: float = 12.0, nthreads=None):
     units = sc.units * reps
     bytes_ = units * ledger.unit_bytes_alg(cfg.S, cfg.d, cfg.r, cfg.k, cfg.elem)
     return {"value": round(bytes_ / dt / 1e9, 4), "unit": "GB/s", "cores": nthreads, "kind": "oracle",
-            "sample": f"{reps} x 1 sequence ({sc.units} units of {cfg.name}, S={cfg.S}, k={cfg.k}) "
+            "sample": f"{reps} x {sc.B} sequences ({sc.units} units of {cfg.name}, S={cfg.S}, k={cfg.k}), "
                       f"Algorithm 1 in plain fp32 C, {dt:.1f} s",
             "us_per_unit": round(dt / units * 1e6, 1)}
 
@@ -442,7 +490,9 @@ def run_reference(args, dist):
     import oracle
     full = synth.CONFIGS[args.config]
     nthreads = os.cpu_count() or 1
-    sc, q, K, V, L, C, sl = oracle_sample(full, 1, seed=full.seed_base + 777)
+    n_seq = max(1, -(-nthreads // full.Hkv))
+    sc, q, K, V, L, C, sl = oracle_sample(full, n_seq, seed=full.seed_base + 777)
+    nthreads = min(nthreads, sc.units)
     t = time.perf_counter()
     oracle.decode_batch(q, K, V, L, C, sl, full.k, nthreads=nthreads)
     pilot = time.perf_counter() - t
@@ -458,7 +508,7 @@ def run_reference(args, dist):
     units = sc.units * reps * args.steps
     value = units * ledger.unit_bytes_alg(full.S, full.d, full.r, full.k, full.elem) / dt / 1e9
     ms_step = dt / args.steps * 1e3
-    sample = f"{reps} x 1 sequence ({sc.units} units) of {full.name} per step, plain fp32 C oracle"
+    sample = f"{reps} x {sc.B} sequences ({sc.units} units) of {full.name} per step, plain fp32 C oracle"
     return {"metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": full.dtype, "data": "synthetic",
