@@ -38,6 +38,9 @@
 #include "ds_common.cuh"
 #include "ds_internal.h"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace ds {
 namespace fused {
 
@@ -46,6 +49,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kAttWarps = 16;  // warps [0, 16): attention; [16, 32): selection tail
 constexpr int kAttThreads = kAttWarps * 32;
 constexpr int kSelThreads = kThreads - kAttThreads;
+constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kUnroll = 8;
 constexpr int kMaxS = 32768;
 constexpr int kMaxR = 256;
@@ -56,10 +60,10 @@ constexpr int kCandCap = 2048;        // digit-1 boundary tokens listed
 constexpr int kMaxMembers = 512;      // 22-bit-prefix boundary tokens ranked directly
 constexpr int kListCap = 2048;        // pool rows per attention round
 constexpr int kBatch = 8;             // rows per warp batch
-constexpr int kBarAtt = 1, kBarSel = 2, kBarDone = 3;  // named barriers
+constexpr int kBarAtt = 1, kBarSel = 2, kBarDone = 3, kBarRegs = 4;  // named barriers
 // register split after the common phases (64 per thread at launch):
 // attention warpgroups 0-3 grow, selection warpgroups 4-7 shrink
-constexpr int kAttRegs = 88, kSelRegs = 40;
+constexpr int kAttRegs = 88, kSelRegs = 40, kCommonRegs = 64;
 static_assert(kAttThreads * kAttRegs + kSelThreads * kSelRegs <= 65536, "register file");
 
 struct alignas(128) Sh {
@@ -76,7 +80,9 @@ struct alignas(128) Sh {
   uint32_t list[kListCap];     // pool row ids of the current attention round
   uint32_t wtot[kWarps];
   uint32_t state[16];
-  uint32_t ncand, nmem, pad0, pad1;
+  uint32_t cnt[4];             // [3] this CTA's selected count (read remotely)
+  uint32_t ncand, nmem, lower_sel, pad0;
+  uint64_t xbar[4];            // cluster exchange barriers of the selection warps
   alignas(16) uint8_t qt[8 * 128 * 2];  // query rows (heads >= G zero), 16-B chunks swizzled
 };
 
@@ -86,13 +92,36 @@ struct Geo {
   static constexpr int CHN = ROWB / 16;                 // 16-B chunks per row
   static constexpr int STAGE = 2 * kBatch * ROWB;       // K rows then V rows of a batch
   static constexpr int RING = kAttWarps * 2 * STAGE;    // 2 stages per attention warp
-  static constexpr int PART = (2 * kAttWarps * 8 + kAttWarps * 8 * D) * 4;
+  static constexpr int PART = (2 * kAttWarps * 8 + kAttWarps * 8 * D) * 4;  // warp partials
+  static constexpr int CPART = (16 + 8 * D) * 4;                           // then the CTA partial
   static_assert(CHN >= 8, "row swizzle needs >= 8 chunks");
 };
 
 __device__ __forceinline__ uint32_t swz(int row, int ch) { return (uint32_t)((ch ^ (row & 7)) << 4); }
 
-template <typename T, int R, int D>
+// cluster-wide exchange among the selection warps of the nch CTAs of a
+// unit: mbarrier xb of every CTA expects one arrival per CTA.
+__device__ __forceinline__ void xchg_arrive(uint64_t *xb, int nch) {
+  const uint32_t a = smem_u32(xb);
+  for (int cr = 0; cr < nch; ++cr) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(a), "r"(cr));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(ra) : "memory");
+  }
+}
+__device__ __forceinline__ void xchg_wait(uint64_t *xb) {
+  const uint32_t a = smem_u32(xb);
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], 0;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a)
+        : "memory");
+}
+
+template <typename T, int R, int D, bool CL>  // CL: a cluster of CTAs per unit
 __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   using GE = Geo<D>;
   constexpr int ROWB = GE::ROWB, CHN = GE::CHN, STAGE = GE::STAGE;
@@ -101,22 +130,39 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   Sh &sh = *reinterpret_cast<Sh *>(smem);
   uint8_t *region = smem + sizeof(Sh);  // keys, then the attention ring, then the partials
   uint32_t *keys = reinterpret_cast<uint32_t *>(region);
+  cg::cluster_group cluster = cg::this_cluster();
+  const int nch = CL ? (int)cluster.num_blocks() : 1, crank = CL ? (int)cluster.block_rank() : 0;
+  // shared memory of CTA cr of the cluster (the local array without a cluster)
+  auto remote = [&](auto *ptr, int cr) {
+    if constexpr (CL) return cluster.map_shared_rank(ptr, cr);
+    else return ptr;
+  };
   const CacheView &c = p.c;
-  const int unit = blockIdx.x;
+  const int unit = blockIdx.y;
   const int b = unit / c.Hkv, h = unit - (unit / c.Hkv) * c.Hkv;
   const int G = c.G;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   DS_TRACE_AT(1, 0);
+  if (CL && tid == 0) {
+    for (int i = 0; i < 4; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&sh.xbar[i])), "r"(nch) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   pdl_wait();  // label / KV rows may come from the preceding append
-  pdl_trigger();
+  // (dependents are released only after the register split below: a CTA of
+  // the next kernel must not take the registers the selection warps free)
   const int n = c.seq_lens[b];
   const int keff = min(p.k, n);
+  const int t0 = crank * p.chunk;                // this CTA's tokens [t0, t0 + nloc)
+  const int nloc = max(0, min(p.chunk, n - t0));
   T *outp = (T *)p.out + ((size_t)b * c.Hq + (size_t)h * G) * D;
   int32_t *idx = p.idx ? p.idx + (size_t)unit * p.k : nullptr;
-  if (n <= 0) {  // empty sequence: y = 0, nothing selected
-    for (int i = tid; i < G * D; i += kThreads) outp[i] = Elem<T>::from_f(0.f);
-    if (idx)
-      for (int i = tid; i < p.k; i += kThreads) idx[i] = -1;
+  if (n <= 0) {  // empty sequence: y = 0, nothing selected (uniform over the cluster)
+    if (crank == 0) {
+      for (int i = tid; i < G * D; i += kThreads) outp[i] = Elem<T>::from_f(0.f);
+      if (idx)
+        for (int i = tid; i < p.k; i += kThreads) idx[i] = -1;
+    }
     return;
   }
 
@@ -137,9 +183,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   for (int i = tid; i < kD1; i += kThreads) sh.h1[i] = 0;
   for (int i = tid; i < kD2; i += kThreads) sh.h2[i] = 0;
   for (int i = tid; i < kMaxS / 32; i += kThreads) sh.selm[i] = 0;
+  if (tid < 4) sh.cnt[tid] = 0;
   if (tid == 0) {
     sh.ncand = 0;
     sh.nmem = 0;
+    sh.lower_sel = 0;
   }
   __syncthreads();
   float ql[R > 0 ? R : 1];
@@ -149,13 +197,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   }
   const float *qs = R > 0 ? ql : sh.qlab;
 
-  // ---- a2: stream the label rows -> order keys + digit-1 histogram
-  const T *lab = (const T *)c.label + ((size_t)b * c.Hkv + h) * (size_t)c.Smax * (size_t)c.r;
+  // ---- a2: stream this CTA's label rows -> order keys + digit-1 histogram
+  const T *lab = (const T *)c.label + (((size_t)b * c.Hkv + h) * (size_t)c.Smax + t0) * (size_t)c.r;
   {
     int i0 = tid;
     if constexpr (R > 0 && R * sizeof(T) == 16) {
       constexpr int U = kUnroll;
-      for (; i0 + (U - 1) * kThreads < n; i0 += U * kThreads) {
+      for (; i0 + (U - 1) * kThreads < nloc; i0 += U * kThreads) {
         uint4 v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) v[u] = __ldg(reinterpret_cast<const uint4 *>(lab) + (size_t)(i0 + u * kThreads));
@@ -171,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         }
       }
     }
-    for (int i = i0; i < n; i += kThreads) {
+    for (int i = i0; i < nloc; i += kThreads) {
       const T *row = lab + (size_t)i * r;
       float s = 0.0f;
       for (int j = 0; j < r; ++j) s = fmaf(qs[j], Elem<T>::to_f(row[j]), s);
@@ -180,29 +228,48 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       atomicAdd(&sh.h1[k0 >> kSh1], 1u);
     }
   }
-  if (tid < 128) keys[n + tid] = 0u;  // pad: below every finite score's key
+  if (tid < 128) keys[nloc + tid] = 0u;  // pad: below every finite score's key
   __syncthreads();
   DS_TRACE_AT(1, 1);
 
-  // ---- a3 level 1: boundary digit D1
-  const bool all_sel = keff >= n;
-  const int ngrp = (n + 31) >> 5;
+  // ---- a3 level 1: boundary digit D1 of the cluster histogram
+  const bool all_sel = keff >= n;  // (uniform over the cluster)
+  // every CTA's mbarriers are initialised and its h1 / c1 complete (read
+  // remotely until the first exchange) before any CTA goes on
+  if (CL && !all_sel) {
+    const uint4 f = reinterpret_cast<const uint4 *>(sh.h1)[tid];  // 64 coarse bins of 64
+    uint32_t v = f.x + f.y + f.z + f.w;
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((tid & 15) == 0) sh.c1[tid >> 4] = v;
+  }
+  if constexpr (CL) cluster.sync();
+  const int ngrp = (nloc + 31) >> 5;
   uint32_t D1 = 0, need1 = 0;
   bool whole1 = true, ovf = false;
   if (!all_sel) {
-    {  // 64 coarse bins of 64: 4 bins per thread, 16 lanes per coarse bin
+    if (!CL) {  // 64 coarse bins of 64: 4 bins per thread, 16 lanes per coarse bin
       const uint4 f = reinterpret_cast<const uint4 *>(sh.h1)[tid];
       uint32_t v = f.x + f.y + f.z + f.w;
 #pragma unroll
       for (int o = 1; o < 16; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if ((tid & 15) == 0) sh.c1[tid >> 4] = v;
+      __syncthreads();
     }
-    __syncthreads();
     if (warp == 0) {
-      uint32_t v[2] = {sh.c1[63 - 2 * lane], sh.c1[62 - 2 * lane]};
+      uint32_t v[2] = {0u, 0u};
+      for (int cr = 0; cr < nch; ++cr) {
+        const uint32_t *rc = remote(sh.c1, cr);
+        v[0] += rc[63 - 2 * lane];
+        v[1] += rc[62 - 2 * lane];
+      }
       const Boundary<2> cb = warp_boundary<2>(v, 63, 0u, (uint32_t)keff);
-      v[0] = sh.h1[cb.bin * 64 + 63 - 2 * lane];
-      v[1] = sh.h1[cb.bin * 64 + 62 - 2 * lane];
+      v[0] = v[1] = 0u;
+      for (int cr = 0; cr < nch; ++cr) {
+        const uint32_t *rf = remote(sh.h1, cr) + cb.bin * 64;
+        v[0] += rf[63 - 2 * lane];
+        v[1] += rf[62 - 2 * lane];
+      }
       const Boundary<2> fb = warp_boundary<2>(v, cb.bin * 64 + 63, cb.above, (uint32_t)keff);
       if (lane == 0) {
         sh.state[0] = (uint32_t)fb.bin;
@@ -214,19 +281,20 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     D1 = sh.state[0];
     need1 = (uint32_t)keff - sh.state[1];
     whole1 = sh.state[2] == need1;
-    ovf = !whole1 && sh.state[2] > (uint32_t)kCandCap;
+    ovf = !whole1 && sh.h1[D1] > (uint32_t)kCandCap;  // this CTA's D1 tokens do not fit the list
   }
+  DS_TRACE_AT(1, 7);
   const bool tail = !all_sel && !whole1;
 
   // ---- masks: per 32-token group, ballot of digit1 > D1 (>= D1 when D1 is
   // taken whole) and digit1 == D1; warp w owns groups of [w*per, w*per+per)
   {
-    int per = (n + kWarps - 1) / kWarps;
+    int per = (nloc + kWarps - 1) / kWarps;
     per = (per + 127) & ~127;
-    const int w0 = min(warp * per, n), w1 = min(w0 + per, n);
+    const int w0 = min(warp * per, nloc), w1 = min(w0 + per, nloc);
     if (all_sel) {
       for (int g = tid; g < ngrp; g += kThreads) {
-        const int rem = n - g * 32;
+        const int rem = nloc - g * 32;
         sh.gtm[g] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
         sh.eqm[g] = 0u;
       }
@@ -249,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         }
       }
       __syncwarp();
+      DS_TRACE_AT(1, 8);
       if (!whole1) {  // the D1 tokens: candidate list + digit-2 histogram (lane per group)
         const int ng = (w1 - w0 + 31) >> 5, grp = (w0 >> 5) + lane;
         uint32_t e = lane < ng ? sh.eqm[grp] : 0u;
@@ -267,41 +336,55 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
           e &= e - 1;
           const uint32_t key = keys[grp * 32 + bit];
           atomicAdd(&sh.h2[(key >> kSh2) & (kD2 - 1)], 1u);
-          if (!ovf) sh.cand[slot++] = make_uint2(key, (uint32_t)(grp * 32 + bit));
+          if (!ovf) sh.cand[slot++] = make_uint2(key, (uint32_t)(t0 + grp * 32 + bit));
         }
       }
     }
   }
+  DS_TRACE_AT(1, 9);
   __syncthreads();
   DS_TRACE_AT(1, 2);
 
   if (warp >= kAttWarps) {
     // ================================================ selection tail
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kSelRegs));
+    named_sync(kBarRegs, kThreads);  // the attention warps hold their registers
+    pdl_trigger();
     const int stid = tid - kAttThreads, sw = warp - kAttWarps;
-    auto for_each_cand = [&](auto &&f) {
+    auto for_each_cand = [&](auto &&f) {  // (key, global token) with digit1 == D1, this CTA
       if (!ovf) {
         const int nc = (int)sh.ncand;
         for (int i = stid; i < nc; i += kSelThreads) f(sh.cand[i].x, (int)sh.cand[i].y);
       } else {  // more D1 tokens than the list holds: scan the keys
-        for (int i = stid; i < n; i += kSelThreads) {
+        for (int i = stid; i < nloc; i += kSelThreads) {
           const uint32_t key = keys[i];
-          if ((key >> kSh1) == D1) f(key, i);
+          if ((key >> kSh1) == D1) f(key, t0 + i);
         }
       }
     };
-    auto mark = [&](int t) { atomicOr(&sh.selm[t >> 5], 1u << (t & 31)); };
-    // coarse sums (32 of 32 bins) of a 1024-bin histogram, then its boundary
-    auto boundary1024 = [&](const uint32_t *hh, uint32_t *cc, uint32_t need, uint32_t *st) {
+    auto mark = [&](int t) { atomicOr(&sh.selm[(t - t0) >> 5], 1u << ((t - t0) & 31)); };
+    auto sel_sync = [&] { named_sync(kBarSel, kSelThreads); };
+    // cluster exchange point x: publish this CTA's data, wait for every CTA's
+    auto exchange = [&](int x) {
+      sel_sync();
+      if constexpr (CL) {
+        if (stid == 0) xchg_arrive(&sh.xbar[x], nch);
+        xchg_wait(&sh.xbar[x]);
+      }
+    };
+    // boundary of a cluster 1024-bin histogram (32 coarse sums of 32 per CTA)
+    auto boundary1024 = [&](uint32_t *hh, uint32_t *cc, uint32_t need, uint32_t *st, int x) {
       uint32_t v = hh[2 * stid] + hh[2 * stid + 1];
 #pragma unroll
       for (int o = 1; o < 16; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if ((stid & 15) == 0) cc[stid >> 4] = v;
-      named_sync(kBarSel, kSelThreads);
+      exchange(x);
       if (sw == 0) {
-        uint32_t w[1] = {cc[31 - lane]};
+        uint32_t w[1] = {0u};
+        for (int cr = 0; cr < nch; ++cr) w[0] += remote(cc, cr)[31 - lane];
         const Boundary<1> cb = warp_boundary<1>(w, 31, 0u, need);
-        w[0] = hh[cb.bin * 32 + 31 - lane];
+        w[0] = 0u;
+        for (int cr = 0; cr < nch; ++cr) w[0] += remote(hh, cr)[cb.bin * 32 + 31 - lane];
         const Boundary<1> fb = warp_boundary<1>(w, cb.bin * 32 + 31, cb.above, need);
         if (lane == 0) {
           st[0] = (uint32_t)fb.bin;
@@ -309,10 +392,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
           st[2] = fb.cnt;
         }
       }
-      named_sync(kBarSel, kSelThreads);
+      sel_sync();
     };
     if (tail) {
-      boundary1024(sh.h2, sh.c2, need1, sh.state + 3);
+      boundary1024(sh.h2, sh.c2, need1, sh.state + 3, 0);
       const uint32_t P2 = (D1 << (kSh1 - kSh2)) | sh.state[3];
       const uint32_t need2 = need1 - sh.state[4];
       const uint32_t cnt2 = sh.state[5];
@@ -323,38 +406,54 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         if (pfx > P2 || (whole2 && pfx == P2)) mark(t);
         else if (pfx == P2 && fits2) sh.members[atomicAdd(&sh.nmem, 1u)] = make_uint2(key, (uint32_t)t);
       });
-      named_sync(kBarSel, kSelThreads);
-      if (!whole2 && fits2) {  // rank by (key desc, token asc)
-        const int nm = (int)cnt2;
+      if (!whole2 && fits2) {
+        exchange(1);  // every CTA's members are listed
+        // the cluster's members land in h2 (no CTA reads it after exchange 1)
+        uint2 *gathered = reinterpret_cast<uint2 *>(sh.h2);
+        static_assert(sizeof(sh.h2) >= kMaxMembers * sizeof(uint2), "member buffer");
+        uint32_t off = 0;
+        for (int cr = 0; cr < nch; ++cr) {
+          const uint32_t m = remote(&sh.nmem, cr)[0];
+          const uint2 *rm = remote(sh.members, cr);
+          for (int i = stid; i < (int)m; i += kSelThreads) gathered[off + i] = rm[i];
+          off += m;
+        }
+        sel_sync();
+        const int nm = (int)cnt2;  // rank by (key desc, token asc)
         for (int i = stid; i < nm; i += kSelThreads) {
-          const uint2 me = sh.members[i];
+          const uint2 me = gathered[i];
           uint32_t rank = 0;
           for (int j = 0; j < nm; ++j) {
-            const uint2 o = sh.members[j];
+            const uint2 o = gathered[j];
             rank += (o.x > me.x) || (o.x == me.x && o.y < me.y);
           }
-          if (rank < need2) mark((int)me.y);
+          if (rank < need2 && (int)me.y >= t0 && (int)me.y < t0 + nloc) mark((int)me.y);
         }
       } else if (!whole2) {
         // massive ties at the 22-bit prefix: digit 3, then token order among
-        // the keys equal to kB (h1 / c1 and eqm are free by now)
+        // the keys equal to kB (h1 / c1 and eqm are no longer read by anyone)
         uint32_t *h3 = sh.h1, *c3 = sh.c1;
         for (int i = stid; i < kD3; i += kSelThreads) h3[i] = 0;
         for (int g = stid; g < ngrp; g += kSelThreads) sh.eqm[g] = 0;
-        named_sync(kBarSel, kSelThreads);
+        sel_sync();
         for_each_cand([&](uint32_t key, int t) {
           if ((key >> kSh2) == P2) atomicAdd(&h3[key & (kD3 - 1)], 1u);
         });
-        named_sync(kBarSel, kSelThreads);
-        boundary1024(h3, c3, need2, sh.state + 6);
+        sel_sync();
+        boundary1024(h3, c3, need2, sh.state + 6, 2);
         const uint32_t kB = (P2 << kSh2) | sh.state[6];
         const uint32_t rem = need2 - sh.state[7];  // keys == kB taken, lowest tokens first
         for_each_cand([&](uint32_t key, int t) {
           if ((key >> kSh2) == P2 && key > kB) mark(t);
-          else if (key == kB) atomicOr(&sh.eqm[t >> 5], 1u << (t & 31));
+          else if (key == kB) atomicOr(&sh.eqm[(t - t0) >> 5], 1u << ((t - t0) & 31));
         });
-        named_sync(kBarSel, kSelThreads);
-        if (sw == 0) {  // token of the rem-th key == kB
+        // keys == kB in lower CTAs (h3 is final on every CTA after exchange 2)
+        uint32_t eq_lower = 0;
+        for (int cr = 0; cr < crank; ++cr) eq_lower += remote(h3, cr)[kB & (kD3 - 1)];
+        const uint32_t my_eq = h3[kB & (kD3 - 1)];
+        const uint32_t take = rem > eq_lower ? min(rem - eq_lower, my_eq) : 0u;
+        sel_sync();
+        if (sw == 0 && take > 0) {  // the take-th local key == kB, token order
           uint32_t run = 0;
           for (int g0 = 0; g0 < ngrp; g0 += 32) {
             const int g = g0 + lane;
@@ -366,26 +465,26 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
               const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
               if (lane >= o) incl += y;
             }
-            if (run + incl >= rem && run + incl - cnt < rem) {
+            if (run + incl >= take && run + incl - cnt < take) {
               uint32_t mm = m;  // drop the set bits before the wanted one
-              for (uint32_t q = run + incl - cnt + 1; q < rem; ++q) mm &= mm - 1;
+              for (uint32_t q = run + incl - cnt + 1; q < take; ++q) mm &= mm - 1;
               sh.state[8] = (uint32_t)(g * 32 + __ffs(mm) - 1);
             }
             const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-            if (run + tot >= rem) break;
+            if (run + tot >= take) break;
             run += tot;
           }
         }
-        named_sync(kBarSel, kSelThreads);
-        const int tB = (int)sh.state[8];
+        sel_sync();
+        const int lB = take == 0 ? -1 : (int)sh.state[8];  // local index of the last taken key == kB
         for (int g = stid; g < ngrp; g += kSelThreads) {
           const uint32_t m = sh.eqm[g];
-          const int t0 = g * 32;
-          const uint32_t le = t0 + 31 <= tB ? 0xffffffffu : (t0 > tB ? 0u : ((2u << (tB - t0)) - 1u));
+          const int l0 = g * 32;
+          const uint32_t le = l0 + 31 <= lB ? 0xffffffffu : (l0 > lB ? 0u : ((2u << (lB - l0)) - 1u));
           if (m & le) atomicOr(&sh.selm[g], m & le);
         }
       }
-      named_sync(kBarSel, kSelThreads);  // every mark is in selm
+      sel_sync();  // every mark is in selm
     }
     named_arrive(kBarDone, kThreads);
     DS_TRACE_BY(1, 3, kAttThreads);
@@ -407,237 +506,322 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       }
       const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31), tb = __shfl_sync(0xffffffffu, ib, 31);
       if (lane == 0) sh.wtot[kAttWarps + sw] = ta + tb;
-      named_sync(kBarSel, kSelThreads);
-      uint32_t base = 0;
-      for (int w = 0; w < sw; ++w) base += sh.wtot[kAttWarps + w];
+      sel_sync();
+      uint32_t base = 0, mine = 0;
+      for (int w = 0; w < kSelWarps; ++w) {
+        const uint32_t x = sh.wtot[kAttWarps + w];
+        if (w < sw) base += x;
+        mine += x;
+      }
+      if (stid == 0) sh.cnt[3] = mine;  // this CTA's selected tokens
+      exchange(3);
+      for (int cr = 0; cr < crank; ++cr) base += remote(sh.cnt, cr)[3];
       uint32_t pa = base + ia - ca, pb = base + ta + ib - cb;
-      for (uint32_t m = ma; m; m &= m - 1) idx[pa++] = ga * 32 + __ffs(m) - 1;
-      for (uint32_t m = mb; m; m &= m - 1) idx[pb++] = gb * 32 + __ffs(m) - 1;
-      for (int i = keff + stid; i < p.k; i += kSelThreads) idx[i] = -1;
+      for (uint32_t m = ma; m; m &= m - 1) idx[pa++] = t0 + ga * 32 + __ffs(m) - 1;
+      for (uint32_t m = mb; m; m &= m - 1) idx[pb++] = t0 + gb * 32 + __ffs(m) - 1;
+      if (crank == 0)
+        for (int i = keff + stid; i < p.k; i += kSelThreads) idx[i] = -1;
     }
-    return;
-  }
-
-  // ================================================== attention warps
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kAttRegs));
-  const int aw = warp;
-  const int gq = lane >> 2, tq = lane & 3;
-  const uint8_t *kp = (const uint8_t *)c.k_pool;
-  const uint8_t *vp = (const uint8_t *)c.v_pool;
-  const int32_t *bt = c.block_table + (size_t)b * c.maxp;
-  const bool pow2 = (c.P & (c.P - 1)) == 0;
-  const int psh = __ffs(c.P) - 1;
-  const float scale = p.scale_log2;
-  uint8_t *ring = region + (size_t)aw * 2 * STAGE;
-  const uint32_t qbase = smem_u32(sh.qt) + (lane & 7) * ROWB;
-  float o[NKS][4];
-#pragma unroll
-  for (int mt = 0; mt < NKS; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
-  float m_run = -INFINITY, l_run = 0.f;
-
-  // one batch of <= 8 rows from stage st (K rows then V rows)
-  auto compute = [&](const uint8_t *st, int nvalid) {
-    float sf[4] = {0.f, 0.f, 0.f, 0.f};
-    const uint32_t kb = smem_u32(st) + (lane & 7) * ROWB;
-#pragma unroll
-    for (int j = 0; j < NKS / 2; ++j) {
-      const int ch = 4 * j + (lane >> 3);
-      uint32_t b0, b1, b2, b3, a0, a2, a0n, a2n;
-      ldmatrix_x4(kb + swz(lane, ch), b0, b1, b2, b3);
-      ldmatrix_x4(qbase + swz(lane, ch), a0, a2, a0n, a2n);
-      const uint32_t A0[4] = {a0, 0u, a2, 0u};
-      const uint32_t A1[4] = {a0n, 0u, a2n, 0u};
-      Mma<T>::run(sf, A0, b0, b1);
-      Mma<T>::run(sf, A1, b2, b3);
+    if constexpr (CL) {  // the attention warps merge the cluster's partials
+      cluster.sync();
+      cluster.sync();
     }
-    // online softmax (base 2) for head gq over rows 2tq, 2tq+1
-    const float z0 = 2 * tq < nvalid ? sf[0] * scale : -INFINITY;
-    const float z1 = 2 * tq + 1 < nvalid ? sf[1] * scale : -INFINITY;
-    float bm = fmaxf(z0, z1);
-    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
-    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
-    const float mnew = fmaxf(m_run, bm);  // finite: row 0 of a batch is valid
-    const float alpha = exp2f(m_run - mnew);
-    const float p0 = exp2f(z0 - mnew), p1 = exp2f(z1 - mnew);
-    l_run = l_run * alpha + p0 + p1;
-    m_run = mnew;
-    const float alo = __shfl_sync(0xffffffffu, alpha, 8 * tq);
-    const float ahi = __shfl_sync(0xffffffffu, alpha, 8 * tq + 4);
+  } else {
+    // ================================================== attention warps
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kAttRegs));
+    named_arrive(kBarRegs, kThreads);
+    pdl_trigger();
+    const int aw = warp;
+    const int gq = lane >> 2, tq = lane & 3;
+    const uint8_t *kp = (const uint8_t *)c.k_pool;
+    const uint8_t *vp = (const uint8_t *)c.v_pool;
+    const int32_t *bt = c.block_table + (size_t)b * c.maxp;
+    const bool pow2 = (c.P & (c.P - 1)) == 0;
+    const int psh = __ffs(c.P) - 1;
+    const float scale = p.scale_log2;
+    uint8_t *ring = region + (size_t)aw * 2 * STAGE;
+    const uint32_t qbase = smem_u32(sh.qt) + (lane & 7) * ROWB;
+    float o[NKS][4];
+#pragma unroll
+    for (int mt = 0; mt < NKS; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;
+
+    // one batch of <= 8 rows from stage st (K rows then V rows)
+    auto compute = [&](const uint8_t *st, int nvalid) {
+      float sf[4] = {0.f, 0.f, 0.f, 0.f};
+      const uint32_t kb = smem_u32(st) + (lane & 7) * ROWB;
+#pragma unroll
+      for (int j = 0; j < NKS / 2; ++j) {
+        const int ch = 4 * j + (lane >> 3);
+        uint32_t b0, b1, b2, b3, a0, a2, a0n, a2n;
+        ldmatrix_x4(kb + swz(lane, ch), b0, b1, b2, b3);
+        ldmatrix_x4(qbase + swz(lane, ch), a0, a2, a0n, a2n);
+        const uint32_t A0[4] = {a0, 0u, a2, 0u};
+        const uint32_t A1[4] = {a0n, 0u, a2n, 0u};
+        Mma<T>::run(sf, A0, b0, b1);
+        Mma<T>::run(sf, A1, b2, b3);
+      }
+      // online softmax (base 2) for head gq over rows 2tq, 2tq+1
+      const float z0 = 2 * tq < nvalid ? sf[0] * scale : -INFINITY;
+      const float z1 = 2 * tq + 1 < nvalid ? sf[1] * scale : -INFINITY;
+      float bm = fmaxf(z0, z1);
+      bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
+      bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
+      const float mnew = fmaxf(m_run, bm);  // finite: row 0 of a batch is valid
+      const float alpha = exp2f(m_run - mnew);
+      const float p0 = exp2f(z0 - mnew), p1 = exp2f(z1 - mnew);
+      l_run = l_run * alpha + p0 + p1;
+      m_run = mnew;
+      const float alo = __shfl_sync(0xffffffffu, alpha, 8 * tq);
+      const float ahi = __shfl_sync(0xffffffffu, alpha, 8 * tq + 4);
+#pragma unroll
+      for (int mt = 0; mt < NKS; ++mt) {
+        o[mt][0] *= alo;
+        o[mt][1] *= ahi;
+        o[mt][2] *= alo;
+        o[mt][3] *= ahi;
+      }
+      const uint32_t bp = pack2<T>(p0, p1);
+      const uint32_t vb = smem_u32(st + kBatch * ROWB) + (lane & 7) * ROWB;
+#pragma unroll
+      for (int j = 0; j < NKS / 2; ++j) {
+        uint32_t v0, v1, v2, v3;
+        ldmatrix_x4_trans(vb + swz(lane, 4 * j + (lane >> 3)), v0, v1, v2, v3);
+        Mma8<T>::run(o[2 * j], v0, v1, bp);
+        Mma8<T>::run(o[2 * j + 1], v2, v3, bp);
+      }
+    };
+
+    // attention over this CTA's rows whose group masks are mask(g), in rounds of kListCap
+    auto run_rows = [&](auto &&mask) {
+      const int ga = aw * 64 + lane, gb = ga + 32;  // warp aw: groups [64 aw, 64 aw + 64)
+      const uint32_t ma = ga < ngrp ? mask(ga) : 0u;
+      const uint32_t mb = gb < ngrp ? mask(gb) : 0u;
+      const uint32_t ca = __popc(ma), cb = __popc(mb);
+      uint32_t ia = ca, ib = cb;
+#pragma unroll
+      for (int o2 = 1; o2 < 32; o2 <<= 1) {
+        const uint32_t ya = __shfl_up_sync(0xffffffffu, ia, o2);
+        const uint32_t yb = __shfl_up_sync(0xffffffffu, ib, o2);
+        if (lane >= o2) {
+          ia += ya;
+          ib += yb;
+        }
+      }
+      const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31), tb = __shfl_sync(0xffffffffu, ib, 31);
+      if (lane == 0) sh.wtot[aw] = ta + tb;
+      named_sync(kBarAtt, kAttThreads);
+      uint32_t base = 0, total = 0;
+      for (int w = 0; w < kAttWarps; ++w) {
+        const uint32_t x = sh.wtot[w];
+        if (w < aw) base += x;
+        total += x;
+      }
+      named_sync(kBarAtt, kAttThreads);  // wtot read by all before any reuse
+      for (uint32_t r0 = 0; r0 < total; r0 += kListCap) {
+        // row ids of list positions [r0, r0 + kListCap)
+        auto put = [&](uint32_t pos, int t) {
+          if (pos >= r0 && pos < r0 + kListCap) {
+            const int pg = pow2 ? (t >> psh) : t / c.P;
+            const int sl = t - pg * c.P;
+            sh.list[pos - r0] =
+                ((uint32_t)__ldg(bt + pg) * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P + (uint32_t)sl;
+          }
+        };
+        uint32_t pa = base + ia - ca, pb = base + ta + ib - cb;
+        for (uint32_t m = ma; m; m &= m - 1) put(pa++, t0 + ga * 32 + __ffs(m) - 1);
+        for (uint32_t m = mb; m; m &= m - 1) put(pb++, t0 + gb * 32 + __ffs(m) - 1);
+        named_sync(kBarAtt, kAttThreads);
+        const int nl = (int)min((uint32_t)kListCap, total - r0);
+        int per = (nl + kAttWarps - 1) / kAttWarps;
+        per = (per + kBatch - 1) & ~(kBatch - 1);
+        const int lo = min(aw * per, nl), hi = min(lo + per, nl);
+        const int nb = (hi - lo + kBatch - 1) / kBatch;
+        auto issue = [&](int j) {
+          uint8_t *st = ring + (j & 1) * STAGE;
+          const int rb = lo + j * kBatch;
+#pragma unroll
+          for (int m = 0; m < kBatch * CHN / 32; ++m) {
+            const int q = lane + 32 * m;
+            const int rr = q / CHN, ch = q % CHN;
+            const bool rv = rb + rr < hi;
+            const size_t off = rv ? (size_t)sh.list[rb + rr] * ROWB + (size_t)ch * 16 : 0;
+            const uint32_t dst = smem_u32(st + rr * ROWB + swz(rr, ch));
+            cp_async16(dst, kp + off, rv ? 16 : 0);
+            cp_async16(dst + kBatch * ROWB, vp + off, rv ? 16 : 0);
+          }
+        };
+        if (nb > 0) issue(0);
+        cp_async_commit();
+        for (int j = 0; j < nb; ++j) {
+          if (j + 1 < nb) issue(j + 1);
+          cp_async_commit();
+          cp_async_wait<1>();
+          __syncwarp();
+          compute(ring + (j & 1) * STAGE, min(kBatch, hi - (lo + j * kBatch)));
+          __syncwarp();  // stage fully read before it is refilled
+        }
+        cp_async_wait<0>();
+        named_sync(kBarAtt, kAttThreads);  // list consumed before the next round
+      }
+    };
+
+    if (!ovf) {
+      run_rows([&](int g) { return sh.gtm[g]; });  // certainly selected: digit1 above D1
+      named_sync(kBarDone, kThreads);              // the selection tail is done
+      DS_TRACE_AT(1, 4);
+      if (tail) run_rows([&](int g) { return sh.selm[g]; });
+    } else {  // the tail still scans the keys in this buffer: wait, then all rows
+      named_sync(kBarDone, kThreads);
+      run_rows([&](int g) { return sh.gtm[g] | sh.selm[g]; });
+    }
+    DS_TRACE_AT(1, 5);
+
+    // ---- warp partials (m, l per head; O^T fragments) -> CTA partial
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+    float *wm = reinterpret_cast<float *>(region);  // [16][8]
+    float *wl = wm + kAttWarps * 8;                 // [16][8]
+    float *wo = wl + kAttWarps * 8;                 // [16][8][D]
+    named_sync(kBarAtt, kAttThreads);               // ring no longer read
+    if (tq == 0) {
+      wm[aw * 8 + gq] = m_run;
+      wl[aw * 8 + gq] = l_run;
+    }
 #pragma unroll
     for (int mt = 0; mt < NKS; ++mt) {
-      o[mt][0] *= alo;
-      o[mt][1] *= ahi;
-      o[mt][2] *= alo;
-      o[mt][3] *= ahi;
+      float *w0 = wo + (size_t)(aw * 8 + 2 * tq) * D + 16 * mt + gq;
+      w0[0] = o[mt][0];
+      w0[D] = o[mt][1];
+      w0[8] = o[mt][2];
+      w0[D + 8] = o[mt][3];
     }
-    const uint32_t bp = pack2<T>(p0, p1);
-    const uint32_t vb = smem_u32(st + kBatch * ROWB) + (lane & 7) * ROWB;
-#pragma unroll
-    for (int j = 0; j < NKS / 2; ++j) {
-      uint32_t v0, v1, v2, v3;
-      ldmatrix_x4_trans(vb + swz(lane, 4 * j + (lane >> 3)), v0, v1, v2, v3);
-      Mma8<T>::run(o[2 * j], v0, v1, bp);
-      Mma8<T>::run(o[2 * j + 1], v2, v3, bp);
-    }
-  };
-
-  // attention over the rows whose group masks are mask(g), in rounds of kListCap
-  auto run_rows = [&](auto &&mask) {
-    const int ga = aw * 64 + lane, gb = ga + 32;  // warp aw: groups [64 aw, 64 aw + 64)
-    const uint32_t ma = ga < ngrp ? mask(ga) : 0u;
-    const uint32_t mb = gb < ngrp ? mask(gb) : 0u;
-    const uint32_t ca = __popc(ma), cb = __popc(mb);
-    uint32_t ia = ca, ib = cb;
-#pragma unroll
-    for (int o2 = 1; o2 < 32; o2 <<= 1) {
-      const uint32_t ya = __shfl_up_sync(0xffffffffu, ia, o2);
-      const uint32_t yb = __shfl_up_sync(0xffffffffu, ib, o2);
-      if (lane >= o2) {
-        ia += ya;
-        ib += yb;
-      }
-    }
-    const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31), tb = __shfl_sync(0xffffffffu, ib, 31);
-    if (lane == 0) sh.wtot[aw] = ta + tb;
     named_sync(kBarAtt, kAttThreads);
-    uint32_t base = 0, total = 0;
-    for (int w = 0; w < kAttWarps; ++w) {
-      const uint32_t x = sh.wtot[w];
-      if (w < aw) base += x;
-      total += x;
-    }
-    named_sync(kBarAtt, kAttThreads);  // wtot read by all before any reuse
-    for (uint32_t r0 = 0; r0 < total; r0 += kListCap) {
-      // row ids of list positions [r0, r0 + kListCap)
-      auto put = [&](uint32_t pos, int t) {
-        if (pos >= r0 && pos < r0 + kListCap) {
-          const int pg = pow2 ? (t >> psh) : t / c.P;
-          const int sl = t - pg * c.P;
-          sh.list[pos - r0] = ((uint32_t)__ldg(bt + pg) * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P + (uint32_t)sl;
+    float *cm = reinterpret_cast<float *>(region + GE::PART);  // [8] m, [8] l, [8][D] o of this CTA
+    for (int i = tid; i < G * D; i += kAttThreads) {
+      const int g = i / D, dd = i - (i / D) * D;
+      float M = -INFINITY;
+#pragma unroll 4
+      for (int w = 0; w < kAttWarps; ++w) M = fmaxf(M, wm[w * 8 + g]);
+      float L = 0.f, O = 0.f;
+      if (M != -INFINITY) {
+#pragma unroll 4
+        for (int w = 0; w < kAttWarps; ++w) {
+          const float sw = exp2f(wm[w * 8 + g] - M);
+          L = fmaf(wl[w * 8 + g], sw, L);
+          O = fmaf(wo[(size_t)(w * 8 + g) * D + dd], sw, O);
         }
-      };
-      uint32_t pa = base + ia - ca, pb = base + ta + ib - cb;
-      for (uint32_t m = ma; m; m &= m - 1) put(pa++, ga * 32 + __ffs(m) - 1);
-      for (uint32_t m = mb; m; m &= m - 1) put(pb++, gb * 32 + __ffs(m) - 1);
-      named_sync(kBarAtt, kAttThreads);
-      const int nl = (int)min((uint32_t)kListCap, total - r0);
-      int per = (nl + kAttWarps - 1) / kAttWarps;
-      per = (per + kBatch - 1) & ~(kBatch - 1);
-      const int lo = min(aw * per, nl), hi = min(lo + per, nl);
-      const int nb = (hi - lo + kBatch - 1) / kBatch;
-      auto issue = [&](int j) {
-        uint8_t *st = ring + (j & 1) * STAGE;
-        const int rb = lo + j * kBatch;
-#pragma unroll
-        for (int m = 0; m < kBatch * CHN / 32; ++m) {
-          const int q = lane + 32 * m;
-          const int rr = q / CHN, ch = q % CHN;
-          const bool rv = rb + rr < hi;
-          const size_t off = rv ? (size_t)sh.list[rb + rr] * ROWB + (size_t)ch * 16 : 0;
-          const uint32_t dst = smem_u32(st + rr * ROWB + swz(rr, ch));
-          cp_async16(dst, kp + off, rv ? 16 : 0);
-          cp_async16(dst + kBatch * ROWB, vp + off, rv ? 16 : 0);
-        }
-      };
-      if (nb > 0) issue(0);
-      cp_async_commit();
-      for (int j = 0; j < nb; ++j) {
-        if (j + 1 < nb) issue(j + 1);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncwarp();
-        compute(ring + (j & 1) * STAGE, min(kBatch, hi - (lo + j * kBatch)));
-        __syncwarp();  // stage fully read before it is refilled
       }
-      cp_async_wait<0>();
-      named_sync(kBarAtt, kAttThreads);  // list consumed before the next round
+      if constexpr (!CL) {
+        outp[i] = Elem<T>::from_f(O / L);
+      } else {
+        cm[16 + i] = O;
+        if (dd == 0) {
+          cm[g] = M;
+          cm[8 + g] = L;
+        }
+      }
     }
-  };
-
-  if (!ovf) {
-    run_rows([&](int g) { return sh.gtm[g]; });  // certainly selected: digit1 above D1
-    named_sync(kBarDone, kThreads);              // the selection tail is done
-    DS_TRACE_AT(1, 4);
-    if (tail) run_rows([&](int g) { return sh.selm[g]; });
-  } else {  // the tail still scans the keys in this buffer: wait, then all rows
-    named_sync(kBarDone, kThreads);
-    run_rows([&](int g) { return sh.gtm[g] | sh.selm[g]; });
-  }
-  DS_TRACE_AT(1, 5);
-
-  // ---- merge the warp partials (m, l per head; O^T fragments) and store y
-  l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
-  l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
-  float *wm = reinterpret_cast<float *>(region);  // [16][8]
-  float *wl = wm + kAttWarps * 8;                 // [16][8]
-  float *wo = wl + kAttWarps * 8;                 // [16][8][D]
-  named_sync(kBarAtt, kAttThreads);               // ring no longer read
-  if (tq == 0) {
-    wm[aw * 8 + gq] = m_run;
-    wl[aw * 8 + gq] = l_run;
-  }
-#pragma unroll
-  for (int mt = 0; mt < NKS; ++mt) {
-    float *w0 = wo + (size_t)(aw * 8 + 2 * tq) * D + 16 * mt + gq;
-    w0[0] = o[mt][0];
-    w0[D] = o[mt][1];
-    w0[8] = o[mt][2];
-    w0[D + 8] = o[mt][3];
-  }
-  named_sync(kBarAtt, kAttThreads);
-  for (int i = tid; i < G * D; i += kAttThreads) {
-    const int g = i / D, dd = i - (i / D) * D;
-    float M = -INFINITY;
-#pragma unroll 4
-    for (int w = 0; w < kAttWarps; ++w) M = fmaxf(M, wm[w * 8 + g]);
-    float L = 0.f, O = 0.f;
-#pragma unroll 4
-    for (int w = 0; w < kAttWarps; ++w) {
-      const float sw = exp2f(wm[w * 8 + g] - M);
-      L = fmaf(wl[w * 8 + g], sw, L);
-      O = fmaf(wo[(size_t)(w * 8 + g) * D + dd], sw, O);
+    // ---- the cluster's partials -> y (CTA cr finishes a slice of the G*D outputs)
+    if constexpr (CL) {
+      cluster.sync();  // every CTA's partial is complete
+      const float *cm0 = reinterpret_cast<const float *>(region + GE::PART);
+      const int per_cta = (G * D + nch - 1) / nch;
+      const int i0 = crank * per_cta, i1 = min(i0 + per_cta, G * D);
+      for (int i = i0 + tid; i < i1; i += kAttThreads) {
+        const int g = i / D;
+        float M = -INFINITY;
+        for (int cr = 0; cr < nch; ++cr) M = fmaxf(M, cluster.map_shared_rank(cm0, cr)[g]);
+        float L = 0.f, O = 0.f;
+        for (int cr = 0; cr < nch; ++cr) {
+          const float *rm = cluster.map_shared_rank(cm0, cr);
+          const float sw = exp2f(rm[g] - M);
+          L = fmaf(rm[8 + g], sw, L);
+          O = fmaf(rm[16 + i], sw, O);
+        }
+        outp[i] = Elem<T>::from_f(O / L);
+      }
+      cluster.sync();  // partials and exchange data stay alive until every reader is done
     }
-    outp[i] = Elem<T>::from_f(O / L);
   }
   DS_TRACE_AT(1, 6);
 }
 
 template <typename T, int R, int D>
-static size_t smem_bytes(const ds_cache *c) {
-  size_t region = ((size_t)c->max_seq_len + 128) * 4;
+static size_t smem_bytes(int chunk) {
+  size_t region = ((size_t)chunk + 128) * 4;
   region = region > (size_t)Geo<D>::RING ? region : (size_t)Geo<D>::RING;
-  region = region > (size_t)Geo<D>::PART ? region : (size_t)Geo<D>::PART;
+  region = region > (size_t)(Geo<D>::PART + Geo<D>::CPART) ? region : (size_t)(Geo<D>::PART + Geo<D>::CPART);
   return sizeof(Sh) + region;
 }
 
-template <typename T, int R, int D>
-static cudaError_t launch_t(const ds_cache *c, const FusedParams &p, cudaStream_t st) {
-  const size_t smem = smem_bytes<T, R, D>(c);
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      decode_kernel<T, R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedMaxSmem);
+template <typename T, int R, int D, bool CL>
+static cudaError_t launch_cl(const ds_cache *c, const FusedParams &p, int nch, cudaStream_t st) {
+  const size_t smem = smem_bytes<T, R, D>(p.chunk);
+  static const cudaError_t attr = [] {
+    cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, R, D, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kFusedMaxSmem);
+    if (e == cudaSuccess && CL)
+      e = cudaFuncSetAttribute(decode_kernel<T, R, D, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return e;
+  }();
   if (attr != cudaSuccess) return attr;
   if (smem > (size_t)kFusedMaxSmem) return cudaErrorInvalidValue;
-  PdlLaunch L(dim3(c->batch * c->num_kv_heads), dim3(kThreads), smem, st);
-  return L.run(decode_kernel<T, R, D>, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nch, c->batch * c->num_kv_heads);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute a[2];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = nch;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = CL ? a : a + 1;  // no cluster attribute for one CTA per unit
+  cfg.numAttrs = CL ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, decode_kernel<T, R, D, CL>, p);
+}
+
+template <typename T, int R, int D>
+static cudaError_t launch_t(const ds_cache *c, const FusedParams &p, int nch, cudaStream_t st) {
+  return nch > 1 ? launch_cl<T, R, D, true>(c, p, nch, st) : launch_cl<T, R, D, false>(c, p, nch, st);
 }
 
 }  // namespace fused
 
-bool fused_applicable(const ds_cache *c) {
-  if (c->dtype != DS_BF16 && c->dtype != DS_FP16) return false;
-  if (c->max_seq_len > fused::kMaxS || c->r > fused::kMaxR) return false;
+// CTAs per unit (one thread-block cluster): enough to cover the SMs when
+// there are few units, enough to hold S keys on chip when S is long.
+int fused_cluster(const ds_cache *c) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // one CTA per unit: worth it once the units cover most of the SMs
-  return c->batch * c->num_kv_heads * 4 >= sms * 3;
+  const int units = c->batch * c->num_kv_heads;
+  int nch = units * 4 >= sms * 3 ? 1 : sms / units;
+  if (nch > 8) nch = 8;
+  const int need = (c->max_seq_len + fused::kMaxS - 1) / fused::kMaxS;
+  if (nch < need) nch = need;
+  if (nch < 1) nch = 1;
+  return nch;
 }
 
-cudaError_t launch_fused(const ds_cache *c, const FusedParams &p, cudaStream_t st) {
+bool fused_applicable(const ds_cache *c) {
+  if (c->dtype != DS_BF16 && c->dtype != DS_FP16) return false;
+  if (c->r > fused::kMaxR) return false;
+  return fused_cluster(c) <= 16;
+}
+
+cudaError_t launch_fused(const ds_cache *c, FusedParams p, cudaStream_t st) {
   using namespace fused;
-#define DS_F(T)                                                                                   \
-  if (c->head_dim == 64) return c->r == 8 ? launch_t<T, 8, 64>(c, p, st) : launch_t<T, 0, 64>(c, p, st); \
-  return c->r == 8 ? launch_t<T, 8, 128>(c, p, st) : launch_t<T, 0, 128>(c, p, st);
+  const int nch = fused_cluster(c);
+  int chunk = (c->max_seq_len + nch - 1) / nch;
+  chunk = (chunk + 127) & ~127;
+  if (chunk > kMaxS) return cudaErrorInvalidValue;
+  p.chunk = chunk;
+#define DS_F(T)                                                                                         \
+  if (c->head_dim == 64) return c->r == 8 ? launch_t<T, 8, 64>(c, p, nch, st) : launch_t<T, 0, 64>(c, p, nch, st); \
+  return c->r == 8 ? launch_t<T, 8, 128>(c, p, nch, st) : launch_t<T, 0, 128>(c, p, nch, st);
   if (c->dtype == DS_BF16) {
     DS_F(__nv_bfloat16)
   }

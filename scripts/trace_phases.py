@@ -95,3 +95,5 @@ def report1():
             prev = s_
 report(2, ["start", "rowids", "loop done", "cluster sync", "merged"])
 report(1, ["start", "streamed", "masks", "tail done", "gt rows done", "all rows", "merged"])
+report_slots(1, [(1, 7, "D1 boundary"), (7, 8, "mask loop w0"), (8, 9, "cand gather w0"), (9, 2, "sync"),
+                 (2, 3, "tail")])

@@ -23,6 +23,10 @@ def gpu_available():
 
 def pytest_collection_modifyitems(config, items):
     if gpu_available():
+        # a hung kernel must fail its test, not the whole run (pytest-timeout)
+        for it in items:
+            if "gpu" in it.keywords and not it.get_closest_marker("timeout"):
+                it.add_marker(pytest.mark.timeout(600))
         return
     skip = pytest.mark.skip(reason="no CUDA device in this container")
     for it in items:

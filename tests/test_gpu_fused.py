@@ -37,6 +37,7 @@ def ragged(B, S, seed):
 def sample_units(cfg, n=12, seed=0):
     g = np.random.default_rng(seed)
     units = {(0, 0), (1, 0), (2, cfg.Hkv - 1), (3, 1), (cfg.B - 1, cfg.Hkv - 1)}
+    n = min(n, cfg.B * cfg.Hkv)
     while len(units) < n:
         units.add((int(g.integers(cfg.B)), int(g.integers(cfg.Hkv))))
     return sorted(units)
@@ -53,6 +54,10 @@ CASES = [
      "iid"),
     ("k1_bf16", synth.Config("k1", B=16, Hq=32, Hkv=8, d=128, S=1024, r=8, k=1, dtype="bf16"), 1, "iid"),
     ("kS_bf16", synth.Config("kS", B=16, Hq=32, Hkv=8, d=128, S=700, r=8, k=700, dtype="bf16"), 700, "iid"),
+    # few units -> a cluster of CTAs per unit (DSMEM histograms, cluster merge)
+    ("cl4_mha_fp16", synth.Config("c4u", B=4, Hq=32, Hkv=8, d=128, S=6000, r=8, k=375, dtype="fp16"), 375, "iid"),
+    ("cl8_gqa_bf16_d64", synth.Config("c8u", B=4, Hq=8, Hkv=2, d=64, S=9000, r=4, k=500, dtype="bf16",
+                                      page_size=7), 500, "clustered"),
 ]
 
 
@@ -142,13 +147,11 @@ def test_fused_full_density_equals_dense():
 
 
 def test_path_choice():
-    """c3 (the bench shape) takes the single kernel; few units or S > 32K
-    take the cluster path."""
+    """16-bit caches take the single kernel (one CTA per unit for many units,
+    a cluster of CTAs per unit for few units or long sequences); fp32 takes
+    the two-kernel path."""
     small = synth.Config("s", B=2, Hq=8, Hkv=2, d=128, S=1024, r=8, k=64, dtype="bf16")
     lay, cache, _ = build_cache(small)
-    assert ds.ds_decode_launches(cache, 64) == 2
-    big = synth.Config("b", B=16, Hq=32, Hkv=8, d=128, S=1024, r=8, k=64, dtype="bf16")
-    lay, cache, _ = build_cache(big)
     assert ds.ds_decode_launches(cache, 64) == 1
     f32 = synth.Config("f", B=16, Hq=32, Hkv=8, d=128, S=256, r=16, k=16, dtype="fp32")
     lay, cache, _ = build_cache(f32)
