@@ -93,7 +93,7 @@ struct Geo {
   static constexpr int STAGE = 2 * kBatch * ROWB;       // K rows then V rows of a batch
   static constexpr int RING = kAttWarps * 2 * STAGE;    // 2 stages per attention warp
   static constexpr int PART = (2 * kAttWarps * 8 + kAttWarps * 8 * D) * 4;  // warp partials
-  static constexpr int CPART = (16 + 8 * D) * 4;                           // then the CTA partial
+  static constexpr int CPART = (16 + 8 * D + 8 * kAttWarps) * 4;          // then the CTA partial + weights
   static_assert(CHN >= 8, "row swizzle needs >= 8 chunks");
 };
 
@@ -119,6 +119,21 @@ __device__ __forceinline__ void xchg_wait(uint64_t *xb) {
         : "=r"(done)
         : "r"(a)
         : "memory");
+}
+
+// sum over the cluster's CTAs of load(cr): the DSMEM loads of up to 8 CTAs
+// are issued together, so a reduction costs one round trip per 8 CTAs
+template <typename F>
+__device__ __forceinline__ uint32_t cluster_sum(int nch, F &&load) {
+  uint32_t s = 0;
+  for (int c0 = 0; c0 < nch; c0 += 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = c0 + j < nch ? load(c0 + j) : 0u;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[j];
+  }
+  return s;
 }
 
 template <typename T, int R, int D, bool CL>  // CL: a cluster of CTAs per unit
@@ -257,19 +272,15 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       __syncthreads();
     }
     if (warp == 0) {
-      uint32_t v[2] = {0u, 0u};
-      for (int cr = 0; cr < nch; ++cr) {
-        const uint32_t *rc = remote(sh.c1, cr);
-        v[0] += rc[63 - 2 * lane];
-        v[1] += rc[62 - 2 * lane];
-      }
+      // lane l: bins 63-2l, 62-2l of the (coarse, then fine) histogram, as one u64
+      const uint2 *c1p = reinterpret_cast<const uint2 *>(sh.c1) + 31 - lane;
+      uint32_t v[2];
+      v[0] = cluster_sum(nch, [&](int cr) { return remote(c1p, cr)->y; });
+      v[1] = cluster_sum(nch, [&](int cr) { return remote(c1p, cr)->x; });
       const Boundary<2> cb = warp_boundary<2>(v, 63, 0u, (uint32_t)keff);
-      v[0] = v[1] = 0u;
-      for (int cr = 0; cr < nch; ++cr) {
-        const uint32_t *rf = remote(sh.h1, cr) + cb.bin * 64;
-        v[0] += rf[63 - 2 * lane];
-        v[1] += rf[62 - 2 * lane];
-      }
+      const uint2 *h1p = reinterpret_cast<const uint2 *>(sh.h1 + cb.bin * 64) + 31 - lane;
+      v[0] = cluster_sum(nch, [&](int cr) { return remote(h1p, cr)->y; });
+      v[1] = cluster_sum(nch, [&](int cr) { return remote(h1p, cr)->x; });
       const Boundary<2> fb = warp_boundary<2>(v, cb.bin * 64 + 63, cb.above, (uint32_t)keff);
       if (lane == 0) {
         sh.state[0] = (uint32_t)fb.bin;
@@ -380,11 +391,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       if ((stid & 15) == 0) cc[stid >> 4] = v;
       exchange(x);
       if (sw == 0) {
-        uint32_t w[1] = {0u};
-        for (int cr = 0; cr < nch; ++cr) w[0] += remote(cc, cr)[31 - lane];
+        uint32_t w[1];
+        w[0] = cluster_sum(nch, [&](int cr) { return remote(cc, cr)[31 - lane]; });
         const Boundary<1> cb = warp_boundary<1>(w, 31, 0u, need);
-        w[0] = 0u;
-        for (int cr = 0; cr < nch; ++cr) w[0] += remote(hh, cr)[cb.bin * 32 + 31 - lane];
+        w[0] = cluster_sum(nch, [&](int cr) { return remote(hh, cr)[cb.bin * 32 + 31 - lane]; });
         const Boundary<1> fb = warp_boundary<1>(w, cb.bin * 32 + 31, cb.above, need);
         if (lane == 0) {
           st[0] = (uint32_t)fb.bin;
@@ -448,8 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
           else if (key == kB) atomicOr(&sh.eqm[(t - t0) >> 5], 1u << ((t - t0) & 31));
         });
         // keys == kB in lower CTAs (h3 is final on every CTA after exchange 2)
-        uint32_t eq_lower = 0;
-        for (int cr = 0; cr < crank; ++cr) eq_lower += remote(h3, cr)[kB & (kD3 - 1)];
+        const uint32_t eq_lower = cluster_sum(crank, [&](int cr) { return remote(h3, cr)[kB & (kD3 - 1)]; });
         const uint32_t my_eq = h3[kB & (kD3 - 1)];
         const uint32_t take = rem > eq_lower ? min(rem - eq_lower, my_eq) : 0u;
         sel_sync();
@@ -515,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       }
       if (stid == 0) sh.cnt[3] = mine;  // this CTA's selected tokens
       exchange(3);
-      for (int cr = 0; cr < crank; ++cr) base += remote(sh.cnt, cr)[3];
+      base += cluster_sum(crank, [&](int cr) { return remote(sh.cnt, cr)[3]; });
       uint32_t pa = base + ia - ca, pb = base + ta + ib - cb;
       for (uint32_t m = ma; m; m &= m - 1) idx[pa++] = t0 + ga * 32 + __ffs(m) - 1;
       for (uint32_t m = mb; m; m &= m - 1) idx[pb++] = t0 + gb * 32 + __ffs(m) - 1;
@@ -676,7 +685,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       run_rows([&](int g) { return sh.gtm[g] | sh.selm[g]; });
     }
     DS_TRACE_AT(1, 5);
-
     // ---- warp partials (m, l per head; O^T fragments) -> CTA partial
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
@@ -697,30 +705,35 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       w0[D + 8] = o[mt][3];
     }
     named_sync(kBarAtt, kAttThreads);
+    DS_TRACE_AT(1, 10);
     float *cm = reinterpret_cast<float *>(region + GE::PART);  // [8] m, [8] l, [8][D] o of this CTA
+    float *wsc = cm + 16 + 8 * D;                              // [8][16] per-warp weights
+    if (aw < G) {  // warp g: head g's weights over the 16 warps (lane w, w + 16)
+      const int g = aw;
+      const float m0 = lane < kAttWarps ? wm[lane * 8 + g] : -INFINITY;
+      float M = m0;
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
+      const float e0 = (lane < kAttWarps && M != -INFINITY) ? exp2f(m0 - M) : 0.f;
+      float L = lane < kAttWarps ? wl[lane * 8 + g] * e0 : 0.f;
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o2);
+      // single CTA: fold 1/L into the weights; cluster: keep (M, L) for the merge
+      if (lane < kAttWarps) wsc[g * kAttWarps + lane] = CL ? e0 : e0 / L;
+      if (lane == 0) {
+        cm[g] = M;
+        cm[8 + g] = L;
+      }
+    }
+    named_sync(kBarAtt, kAttThreads);
+    DS_TRACE_AT(1, 11);
     for (int i = tid; i < G * D; i += kAttThreads) {
       const int g = i / D, dd = i - (i / D) * D;
-      float M = -INFINITY;
-#pragma unroll 4
-      for (int w = 0; w < kAttWarps; ++w) M = fmaxf(M, wm[w * 8 + g]);
-      float L = 0.f, O = 0.f;
-      if (M != -INFINITY) {
-#pragma unroll 4
-        for (int w = 0; w < kAttWarps; ++w) {
-          const float sw = exp2f(wm[w * 8 + g] - M);
-          L = fmaf(wl[w * 8 + g], sw, L);
-          O = fmaf(wo[(size_t)(w * 8 + g) * D + dd], sw, O);
-        }
-      }
-      if constexpr (!CL) {
-        outp[i] = Elem<T>::from_f(O / L);
-      } else {
-        cm[16 + i] = O;
-        if (dd == 0) {
-          cm[g] = M;
-          cm[8 + g] = L;
-        }
-      }
+      float O = 0.f;
+#pragma unroll
+      for (int w = 0; w < kAttWarps; ++w) O = fmaf(wo[(size_t)(w * 8 + g) * D + dd], wsc[g * kAttWarps + w], O);
+      if constexpr (!CL) outp[i] = Elem<T>::from_f(O);
+      else cm[16 + i] = O;
     }
     // ---- the cluster's partials -> y (CTA cr finishes a slice of the G*D outputs)
     if constexpr (CL) {
@@ -730,14 +743,35 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       const int i0 = crank * per_cta, i1 = min(i0 + per_cta, G * D);
       for (int i = i0 + tid; i < i1; i += kAttThreads) {
         const int g = i / D;
-        float M = -INFINITY;
-        for (int cr = 0; cr < nch; ++cr) M = fmaxf(M, cluster.map_shared_rank(cm0, cr)[g]);
-        float L = 0.f, O = 0.f;
-        for (int cr = 0; cr < nch; ++cr) {
-          const float *rm = cluster.map_shared_rank(cm0, cr);
-          const float sw = exp2f(rm[g] - M);
-          L = fmaf(rm[8 + g], sw, L);
-          O = fmaf(rm[16 + i], sw, O);
+        float M = -INFINITY, L = 0.f, O = 0.f;
+        for (int c0 = 0; c0 < nch; c0 += 8) {  // online merge, 8 CTAs' loads in flight
+          float mm[8], ll[8], oo[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (c0 + j < nch) {
+              const float *rm = cluster.map_shared_rank(cm0, c0 + j);
+              mm[j] = rm[g];
+              ll[j] = rm[8 + g];
+              oo[j] = rm[16 + i];
+            } else {
+              mm[j] = -INFINITY;
+              ll[j] = oo[j] = 0.f;
+            }
+          }
+          float Mn = M;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) Mn = fmaxf(Mn, mm[j]);
+          if (Mn == -INFINITY) continue;  // no rows in these CTAs yet
+          const float a = exp2f(M - Mn);  // M = -inf at first: a = 0 and L = O = 0 anyway
+          L *= a;
+          O *= a;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float sw = exp2f(mm[j] - Mn);
+            L = fmaf(ll[j], sw, L);
+            O = fmaf(oo[j], sw, O);
+          }
+          M = Mn;
         }
         outp[i] = Elem<T>::from_f(O / L);
       }
