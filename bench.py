@@ -32,6 +32,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import synth  # noqa: E402
@@ -58,6 +59,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--extra", action="store_true", help="also time c2 S=4K/16K/32K (reported under 'extra')")
+    ap.add_argument("--offload", action="store_true",
+                    help="Double Sparsity-Offload pipeline on c5 (KV in pinned host memory); prints its own line")
     return ap.parse_args()
 
 
@@ -520,6 +523,100 @@ def run_reference(args, dist):
             "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def run_offload(args, dist):
+    """f1: Double Sparsity-Offload on c5.  K/V pools live in pinned
+    host memory; per layer l, the main stream attends over slot l % 2 (rows
+    prefetched earlier) while the side stream runs ds_prefetch_next_layer for
+    layer l + 1 with a predicted query (cos ~0.95, reading R15) into the other
+    slot.  Timed: exactly K steps of L layers after W warm-up steps (CUDA
+    events on the main stream, after a join with the side stream)."""
+    import paper_2408_07092_b200 as ds
+    dev = torch.device("cuda", dist.local)
+    torch.cuda.set_device(dev)
+    cfg = synth.CONFIGS["c5"]
+    L = min(args.layers, 2)
+    layers = []
+    for l in range(L):
+        seed = cfg.seed_base + l
+        lay = synth.make_layer(cfg, seed, device=dev)
+        cache = ds.LayerCache.allocate(cfg.B, cfg.Hq, cfg.Hkv, cfg.d, cfg.S, cfg.r, synth.DTYPES[cfg.dtype],
+                                       lay.block_table, num_pages=lay.num_pages, page_size=cfg.page_size,
+                                       channel_idx=lay.C_plant, host_kv=True)
+        ds.prefill(cache, lay.K, lay.V, lay.seq_lens)
+        torch.cuda.synchronize()
+        q = lay.q.contiguous()
+        layers.append(dict(cache=cache, q=q, q_hat=synth.predicted_query(q, 0.95, seed), out=torch.empty_like(q)))
+        del lay
+        torch.cuda.empty_cache()
+    slots = [ds.PrefetchSlot.allocate(layers[0]["cache"], cfg.k, dev) for _ in range(2)]
+    main_s, side_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    with torch.cuda.stream(side_s):                      # layer 0's rows before the first step
+        ds.ds_prefetch_next_layer(layers[0]["cache"], layers[0]["q_hat"], cfg.k, slots[0], stream=side_s)
+        ready[0].record(side_s)
+
+    def step(base):
+        for l in range(L):
+            i = base + l
+            s_cur, s_nxt = slots[i % 2], slots[(i + 1) % 2]
+            nxt = layers[(l + 1) % L]
+            with torch.cuda.stream(side_s):              # prefetch layer l+1 (slot freed by layer l-1)
+                side_s.wait_event(free[(i + 1) % 2])
+                ds.ds_prefetch_next_layer(nxt["cache"], nxt["q_hat"], cfg.k, s_nxt, stream=side_s)
+                ready[(i + 1) % 2].record(side_s)
+            with torch.cuda.stream(main_s):              # attention of layer l on its prefetched rows
+                main_s.wait_event(ready[i % 2])
+                ly = layers[l]
+                ds.ds_decode_attention_prefetched(ly["cache"], ly["q"], s_cur, ly["out"], stream=main_s)
+                free[i % 2].record(main_s)
+    for w in range(args.warmup):
+        step(w * L)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(main_s)
+    for st in range(args.steps):
+        step((args.warmup + st) * L)
+    main_s.wait_stream(side_s)
+    e1.record(main_s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    us_layer = ms * 1e3 / L
+    link_bytes = cfg.B * cfg.Hkv * cfg.k * 2 * cfg.d * cfg.elem          # K+V rows per layer over the link
+    # prefetch alone (one layer, side stream idle otherwise)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(side_s):
+        t0.record(side_s)
+        for _ in range(3):
+            ds.ds_prefetch_next_layer(layers[0]["cache"], layers[0]["q_hat"], cfg.k, slots[0], stream=side_s)
+        t1.record(side_s)
+    torch.cuda.synchronize()
+    us_pf = t0.elapsed_time(t1) / 3 * 1e3
+    jac = []
+    idx = torch.empty((cfg.B, cfg.Hkv, cfg.k), dtype=torch.int32, device=dev)
+    ds.ds_decode_attention(layers[0]["cache"], layers[0]["q"], cfg.k, topk_idx_out=idx)
+    ds.ds_prefetch_next_layer(layers[0]["cache"], layers[0]["q_hat"], cfg.k, slots[0])
+    torch.cuda.synchronize()
+    a, b = idx.cpu().numpy(), slots[0].idx.cpu().numpy()
+    for bb in range(cfg.B):
+        for h in range(cfg.Hkv):
+            sa, sb = set(a[bb, h].tolist()), set(b[bb, h].tolist())
+            jac.append(len(sa & sb) / max(1, len(sa | sb)))
+    dev_bytes = sum(x.numel() * x.element_size() for sl in slots for x in (sl.k_rows, sl.v_rows, sl.idx)) + \
+        L * layers[0]["cache"].label.numel() * layers[0]["cache"].label.element_size()
+    return {"metric": "Double Sparsity-Offload decode µs/layer (c5, KV in pinned host memory)",
+            "value": round(us_layer, 2), "unit": "µs/layer", "higher_is_better": False, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "dtype": cfg.dtype, "data": "synthetic",
+            "config": {"workload": f"c5: B={cfg.B} Hq={cfg.Hq} Hkv={cfg.Hkv} d={cfg.d} S={cfg.S} r={cfg.r} "
+                                   f"k={cfg.k} {cfg.dtype}, K/V pools pinned host, {L} layers, q_hat cos 0.95"},
+            "link_bytes_per_layer": link_bytes, "link_gbs": round(link_bytes / (us_layer * 1e-6) / 1e9, 2),
+            "prefetch_alone_us": round(us_pf, 2),
+            "prefetch_alone_link_gbs": round(link_bytes / (us_pf * 1e-6) / 1e9, 2),
+            "jaccard_qhat_vs_q_mean": round(float(np.mean(jac)), 4),
+            "device_bytes_label_plus_slots": int(dev_bytes),
+            "host_kv_bytes_per_layer": int(2 * layers[0]["cache"].k_pool.numel() * cfg.elem)}
+
+
 def main():
     args = parse()
     dist = Dist()
@@ -532,7 +629,7 @@ def main():
         raise SystemExit("bench.py (ours) needs a CUDA device; there is no CPU fallback")
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     dist.init("nccl")
-    res = run_ours(args, dist)
+    res = run_offload(args, dist) if args.offload else run_ours(args, dist)
     if dist.rank == 0:
         print(json.dumps(res), flush=True)
     dist.done()

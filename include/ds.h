@@ -152,6 +152,45 @@ ds_status ds_decode_attention(const ds_cache *c, const void *q, int32_t k, void 
  * are identical up to the fp32 summation order of the attention. */
 int32_t ds_decode_launches(const ds_cache *c, int32_t k);
 
+/* ---------------------------------------------------------------------
+ * Double Sparsity-Offload, Sec. 5.1: "The complete KV cache is
+ * stored on the CPU, while the GPU maintains only the label cache and a
+ * double buffer.  [...] each layer processes its embeddings through the next
+ * layer's query projection to generate an approximate query for the
+ * subsequent layer [...] the tokens corresponding to the approximate
+ * attention results for the next layer are offloaded to the GPU" (reading
+ * R15: the predicted query is an input).
+ *
+ * A slot is one half of the double buffer (caller-allocated device memory):
+ *   idx    int32 [batch][num_kv_heads][k]  selected tokens, ascending, -1 past k_eff
+ *   count  int32 [batch]                   k_eff = min(k, seq_lens[b])
+ *   table  int32 [batch]                   written as 0..batch-1 (the slot's page table)
+ *   k_rows, v_rows [batch][num_kv_heads][k][head_dim]  the gathered K / V rows
+ */
+typedef struct {
+  int32_t k;
+  int32_t *idx, *count, *table;
+  void *k_rows, *v_rows;
+} ds_prefetch_slot;
+
+/* Lines 1-3 of Algorithm 1 with the predicted query q_pred [batch][Hq][d]
+ * against next's device-resident label cache, then the k_eff selected K/V
+ * rows of every unit are copied from next's pools -- pinned host memory
+ * (cudaHostAlloc / torch pin_memory; read over the host link through unified
+ * addressing) or device memory -- into the slot, ascending by token.  Enqueued
+ * on side_stream (typically overlapping the current layer's attention); the
+ * caller orders the consumer after it (an event).  16-bit dtypes only
+ * (DS_ERR_UNSUPPORTED otherwise). */
+ds_status ds_prefetch_next_layer(const ds_cache *next, const void *q_pred, int32_t k,
+                                 const ds_prefetch_slot *slot, cudaStream_t side_stream);
+
+/* Lines 4-5 of Algorithm 1 with the layer's true query q over the rows a
+ * prefetch put in slot: y = softmax(q K_slot^T / sqrt(d)) V_slot, exact, over
+ * the count[b] rows of each unit.  c supplies the shape (its pools are not
+ * read).  out [batch][Hq][d]. */
+ds_status ds_decode_attention_prefetched(const ds_cache *c, const void *q, const ds_prefetch_slot *slot,
+                                         void *out, cudaStream_t stream);
+
 /* Lines 1-2 of Algorithm 1 only, for diagnostics and tests:
  * scores_out fp32 [batch][num_kv_heads][max_seq_len]; entries t >=
  * seq_lens[b] are left untouched.  Same arithmetic as ds_decode_attention. */

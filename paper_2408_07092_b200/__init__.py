@@ -69,6 +69,11 @@ def lib():
         L.ds_decode_workspace_size.restype = SZ
         L.ds_decode_attention.argtypes = [C, P, I32, P, P, P, SZ, P]
         L.ds_approx_scores.argtypes = [C, P, P, P]
+        SL = ctypes.POINTER(ds_prefetch_slot)
+        L.ds_prefetch_next_layer.argtypes = [C, P, I32, SL, P]
+        L.ds_decode_attention_prefetched.argtypes = [C, P, SL, P, P]
+        L.ds_prefetch_next_layer.restype = ctypes.c_int
+        L.ds_decode_attention_prefetched.restype = ctypes.c_int
         L.ds_decode_launches.argtypes = [C, I32]
         L.ds_decode_launches.restype = I32
         L.ds_dense_workspace_size.argtypes = [C]
@@ -83,7 +88,8 @@ def lib():
 
 EXPORTS = ("ds_status_string", "ds_version", "ds_calibrate_channels", "ds_append_kv",
            "ds_decode_workspace_size", "ds_decode_attention", "ds_approx_scores",
-           "ds_dense_workspace_size", "ds_dense_decode_attention", "ds_decode_launches")
+           "ds_dense_workspace_size", "ds_dense_decode_attention", "ds_decode_launches",
+           "ds_prefetch_next_layer", "ds_decode_attention_prefetched")
 
 
 def ds_status_string(s: int) -> str:
@@ -97,8 +103,8 @@ def ds_version() -> str:
 def _ptr(t):
     if t is None:
         return None
-    if not t.is_cuda:
-        raise ValueError("libds takes device tensors (no CPU path)")
+    if not t.is_cuda and not t.is_pinned():  # pinned host memory is device-addressable (offload pools)
+        raise ValueError("libds takes device tensors or pinned host tensors (no CPU path)")
     if not t.is_contiguous():
         raise ValueError("libds takes contiguous tensors")
     return ctypes.c_void_p(t.data_ptr())
@@ -137,13 +143,20 @@ class LayerCache:
 
     @staticmethod
     def allocate(batch, num_q_heads, num_kv_heads, head_dim, max_seq_len, r, dtype, block_table,
-                 num_pages=None, page_size=16, device="cuda", channel_idx=None):
+                 num_pages=None, page_size=16, device="cuda", channel_idx=None, host_kv=False):
+        """host_kv: K/V pools in pinned host memory (Double Sparsity-Offload,
+        P:192): the kernels read them over the host link; label stays on device."""
         bt = torch.as_tensor(block_table, dtype=torch.int32).to(device).contiguous()
         npages = int(num_pages if num_pages is not None else int(bt.max()) + 1)
         pool = (npages, num_kv_heads, page_size, head_dim)
+
+        def pool_buf():
+            if host_kv:
+                return torch.empty(pool, dtype=dtype, pin_memory=True)
+            return torch.empty(pool, dtype=dtype, device=device)
         return LayerCache(
             batch, num_q_heads, num_kv_heads, head_dim, page_size, max_seq_len, r, dtype,
-            torch.empty(pool, dtype=dtype, device=device), torch.empty(pool, dtype=dtype, device=device),
+            pool_buf(), pool_buf(),
             bt, torch.zeros(batch, dtype=torch.int32, device=device),
             torch.empty((batch, num_kv_heads, max_seq_len, r), dtype=dtype, device=device),
             (torch.as_tensor(channel_idx, dtype=torch.int32).to(device).contiguous() if channel_idx is not None
@@ -207,6 +220,56 @@ def ds_decode_attention(cache: LayerCache, q, k, out=None, topk_idx_out=None, ws
     st = lib().ds_decode_attention(ctypes.byref(cs), _ptr(q), k, _ptr(out), _ptr(topk_idx_out), _ptr(ws),
                                    ws.numel(), _stream(stream))
     _check(st, "ds_decode_attention")
+    return out
+
+
+class ds_prefetch_slot(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int32), ("idx", ctypes.c_void_p), ("count", ctypes.c_void_p),
+                ("table", ctypes.c_void_p), ("k_rows", ctypes.c_void_p), ("v_rows", ctypes.c_void_p)]
+
+
+@dataclass
+class PrefetchSlot:
+    """One half of the offload double buffer (ds_prefetch_slot, device memory)."""
+    k: int
+    idx: torch.Tensor
+    count: torch.Tensor
+    table: torch.Tensor
+    k_rows: torch.Tensor
+    v_rows: torch.Tensor
+
+    @staticmethod
+    def allocate(cache: LayerCache, k: int, device="cuda"):
+        B, H, d = cache.batch, cache.num_kv_heads, cache.head_dim
+        return PrefetchSlot(k, torch.empty((B, H, k), dtype=torch.int32, device=device),
+                            torch.zeros(B, dtype=torch.int32, device=device),
+                            torch.zeros(B, dtype=torch.int32, device=device),
+                            torch.empty((B, H, k, d), dtype=cache.dtype, device=device),
+                            torch.empty((B, H, k, d), dtype=cache.dtype, device=device))
+
+    def struct(self) -> ds_prefetch_slot:
+        return ds_prefetch_slot(self.k, _ptr(self.idx), _ptr(self.count), _ptr(self.table), _ptr(self.k_rows),
+                                _ptr(self.v_rows))
+
+
+def ds_prefetch_next_layer(next_cache: LayerCache, q_pred, k, slot: PrefetchSlot = None, stream=None):
+    """a6: select with the predicted query, gather the rows into a device slot."""
+    slot = slot if slot is not None else PrefetchSlot.allocate(next_cache, k, q_pred.device)
+    ss = slot.struct()
+    st = lib().ds_prefetch_next_layer(ctypes.byref(next_cache.struct()), _ptr(q_pred), k, ctypes.byref(ss),
+                                      _stream(stream))
+    _check(st, "ds_prefetch_next_layer")
+    return slot
+
+
+def ds_decode_attention_prefetched(cache: LayerCache, q, slot: PrefetchSlot, out=None, stream=None):
+    """Lines 4-5 with the true query over a prefetched slot."""
+    if out is None:
+        out = torch.empty_like(q)
+    ss = slot.struct()
+    st = lib().ds_decode_attention_prefetched(ctypes.byref(cache.struct()), _ptr(q), ctypes.byref(ss), _ptr(out),
+                                              _stream(stream))
+    _check(st, "ds_decode_attention_prefetched")
     return out
 
 

@@ -157,6 +157,7 @@ ds_status ds_decode_attention(const ds_cache *c, const void *q, int32_t k, void 
     fp.k = k;
     fp.out = out;
     fp.idx = topk_idx_out;
+    fp.select_only = 0;
     fp.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c->head_dim));
     return cuda_status(launch_fused(c, fp, stream));
   }
@@ -194,6 +195,57 @@ ds_status ds_approx_scores(const ds_cache *c, const void *q, float *scores_out, 
   sc.scores = scores_out;
   sc.chunk = sg.chunk;
   return cuda_status(launch_score(c, sc, sg, stream));
+}
+
+static ds_status check_slot(const ds_cache *c, const ds_prefetch_slot *slot) {
+  if (!slot || slot->k < 1 || slot->k > c->max_seq_len) return DS_ERR_INVALID_ARGUMENT;
+  if (!slot->idx || !slot->count || !slot->table || !slot->k_rows || !slot->v_rows) return DS_ERR_INVALID_ARGUMENT;
+  if (!aligned16(slot->k_rows) || !aligned16(slot->v_rows)) return DS_ERR_INVALID_ARGUMENT;
+  if ((long long)c->batch * c->num_kv_heads * slot->k >= (1ll << 31)) return DS_ERR_UNSUPPORTED;
+  return DS_OK;
+}
+
+ds_status ds_prefetch_next_layer(const ds_cache *next, const void *q_pred, int32_t k, const ds_prefetch_slot *slot,
+                                 cudaStream_t side_stream) {
+  ds_status s = validate_cache(next);
+  if (s != DS_OK) return s;
+  if (!q_pred || !aligned16(q_pred)) return DS_ERR_INVALID_ARGUMENT;
+  if ((s = check_slot(next, slot)) != DS_OK) return s;
+  if (k != slot->k) return DS_ERR_INVALID_ARGUMENT;
+  if (!fused_applicable(next)) return DS_ERR_UNSUPPORTED;
+  FusedParams fp;
+  fp.c = make_view(next);
+  fp.q = q_pred;
+  fp.k = k;
+  fp.out = nullptr;
+  fp.idx = slot->idx;
+  fp.scale_log2 = 0.f;
+  fp.select_only = 1;
+  if (launch_fused(next, fp, side_stream) != cudaSuccess) return DS_ERR_CUDA;
+  return cuda_status(launch_gather(next, slot, side_stream));
+}
+
+ds_status ds_decode_attention_prefetched(const ds_cache *c, const void *q, const ds_prefetch_slot *slot, void *out,
+                                         cudaStream_t stream) {
+  ds_status s = validate_cache(c);
+  if (s != DS_OK) return s;
+  if (!q || !out || !aligned16(q) || !aligned16(out)) return DS_ERR_INVALID_ARGUMENT;
+  if ((s = check_slot(c, slot)) != DS_OK) return s;
+  // the slot as a paged cache: one page of k rows per sequence, page b = b
+  ds_cache v = *c;
+  v.page_size = slot->k;
+  v.num_pages = c->batch;
+  v.max_pages_per_seq = 1;
+  v.max_seq_len = slot->k;
+  v.k_pool = slot->k_rows;
+  v.v_pool = slot->v_rows;
+  v.block_table = slot->table;
+  v.seq_lens = slot->count;
+  AttnGeom ag = attn_geom(&v, v.max_seq_len);
+  if (ag.nsplit < 1) return DS_ERR_UNSUPPORTED;
+  AttnParams ap;
+  fill_attn(ap, &v, q, nullptr, 0, ag, out);
+  return cuda_status(launch_attn(&v, ap, ag, stream));
 }
 
 size_t ds_dense_workspace_size(const ds_cache *c) {

@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   int32_t *idx = p.idx ? p.idx + (size_t)unit * p.k : nullptr;
   if (n <= 0) {  // empty sequence: y = 0, nothing selected (uniform over the cluster)
     if (crank == 0) {
-      for (int i = tid; i < G * D; i += kThreads) outp[i] = Elem<T>::from_f(0.f);
+      if (!p.select_only)
+        for (int i = tid; i < G * D; i += kThreads) outp[i] = Elem<T>::from_f(0.f);
       if (idx)
         for (int i = tid; i < p.k; i += kThreads) idx[i] = -1;
     }
@@ -540,6 +541,14 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kAttRegs));
     named_arrive(kBarRegs, kThreads);
     pdl_trigger();
+    if (p.select_only) {  // a6 prefetch: the selection warps write the index list
+      named_sync(kBarDone, kThreads);
+      if constexpr (CL) {
+        cluster.sync();
+        cluster.sync();
+      }
+      return;
+    }
     const int aw = warp;
     const int gq = lane >> 2, tq = lane & 3;
     const uint8_t *kp = (const uint8_t *)c.k_pool;

@@ -48,10 +48,12 @@ struct FusedParams {
   int32_t *idx;      // nullable [units][k]
   float scale_log2;  // log2(e) / sqrt(D)
   int chunk;         // tokens per CTA (cluster of ceil(S / chunk) CTAs per unit)
+  int select_only;   // a6 prefetch: lines 1-3 only (idx written, no attention, out unused)
 };
 constexpr int kFusedMaxSmem = 227 * 1024;
 bool fused_applicable(const ds_cache *c);
 cudaError_t launch_fused(const ds_cache *c, FusedParams p, cudaStream_t st);
+cudaError_t launch_gather(const ds_cache *c, const ds_prefetch_slot *slot, cudaStream_t st);
 int fused_cluster(const ds_cache *c);
 
 // Launch-geometry decisions (deterministic functions of the cache shape).
