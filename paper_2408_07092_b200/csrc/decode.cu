@@ -357,6 +357,17 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   __syncthreads();
   DS_TRACE_AT(1, 2);
 
+  const int32_t *bt = c.block_table + (size_t)b * c.maxp;
+  const bool pow2 = (c.P & (c.P - 1)) == 0;
+  const int psh = __ffs(c.P) - 1;
+  auto row_of = [&](int t) -> uint32_t {  // pool row id of token t (block table lookup)
+    const int pg = pow2 ? (t >> psh) : t / c.P;
+    const int sl = t - pg * c.P;
+    return ((uint32_t)__ldg(bt + pg) * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P + (uint32_t)sl;
+  };
+  if (tid == 0) sh.state[14] = 0u;  // candidate rows not listed yet (read by the attention warps)
+  __syncthreads();
+
   if (warp >= kAttWarps) {
     // ================================================ selection tail
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kSelRegs));
@@ -496,7 +507,56 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       }
       sel_sync();  // every mark is in selm
     }
-    named_arrive(kBarDone, kThreads);
+    if (ovf) {
+      named_arrive(kBarDone, kThreads);  // the attention warps wait for the keys buffer
+    } else {
+      // the selected candidates' row ids go to list positions [n_gt, n_gt + n_sel),
+      // behind the attention warps' own list of the certain rows; then a flag
+      // (no CTA barrier: each attention warp picks them up when it is done)
+      const int ga = sw * 64 + lane, gb = ga + 32;  // warp sw: groups [64 sw, 64 sw + 64)
+      const uint32_t ma = (tail && ga < ngrp) ? sh.selm[ga] : 0u;
+      const uint32_t mb = (tail && gb < ngrp) ? sh.selm[gb] : 0u;
+      uint32_t gt = (ga < ngrp ? __popc(sh.gtm[ga]) : 0u) + (gb < ngrp ? __popc(sh.gtm[gb]) : 0u);
+      const uint32_t ca = __popc(ma), cb = __popc(mb);
+      uint32_t ia = ca, ib = cb;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t ya = __shfl_up_sync(0xffffffffu, ia, o);
+        const uint32_t yb = __shfl_up_sync(0xffffffffu, ib, o);
+        if (lane >= o) {
+          ia += ya;
+          ib += yb;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gt += __shfl_xor_sync(0xffffffffu, gt, o);
+      const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31), tb = __shfl_sync(0xffffffffu, ib, 31);
+      if (lane == 0) {
+        sh.wtot[kAttWarps + sw] = ta + tb;
+        sh.cand[sw].x = gt;  // (the candidate list is no longer read)
+      }
+      sel_sync();
+      uint32_t base = 0, n_sel = 0, n_gt = 0;
+      for (int w = 0; w < kSelWarps; ++w) {
+        const uint32_t x = sh.wtot[kAttWarps + w];
+        if (w < sw) base += x;
+        n_sel += x;
+        n_gt += sh.cand[w].x;
+      }
+      const bool fits = n_gt + n_sel <= (uint32_t)kListCap;
+      if (fits) {
+        uint32_t pa = n_gt + base + ia - ca, pb = n_gt + base + ta + ib - cb;
+        for (uint32_t m = ma; m; m &= m - 1) sh.list[pa++] = row_of(t0 + ga * 32 + __ffs(m) - 1);
+        for (uint32_t m = mb; m; m &= m - 1) sh.list[pb++] = row_of(t0 + gb * 32 + __ffs(m) - 1);
+      }
+      sel_sync();
+      if (stid == 0) {
+        sh.state[12] = n_gt;
+        sh.state[13] = n_sel;
+        __threadfence_block();
+        *reinterpret_cast<volatile uint32_t *>(&sh.state[14]) = fits ? 1u : 2u;
+      }
+    }
     DS_TRACE_BY(1, 3, kAttThreads);
     // ---- optional index list: ascending selected tokens, -1 past k_eff
     if (idx) {
@@ -542,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     named_arrive(kBarRegs, kThreads);
     pdl_trigger();
     if (p.select_only) {  // a6 prefetch: the selection warps write the index list
-      named_sync(kBarDone, kThreads);
+      if (ovf) named_sync(kBarDone, kThreads);  // (matches their arrive)
       if constexpr (CL) {
         cluster.sync();
         cluster.sync();
@@ -553,9 +613,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     const int gq = lane >> 2, tq = lane & 3;
     const uint8_t *kp = (const uint8_t *)c.k_pool;
     const uint8_t *vp = (const uint8_t *)c.v_pool;
-    const int32_t *bt = c.block_table + (size_t)b * c.maxp;
-    const bool pow2 = (c.P & (c.P - 1)) == 0;
-    const int psh = __ffs(c.P) - 1;
     const float scale = p.scale_log2;
     uint8_t *ring = region + (size_t)aw * 2 * STAGE;
     const uint32_t qbase = smem_u32(sh.qt) + (lane & 7) * ROWB;
@@ -610,8 +667,45 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       }
     };
 
-    // attention over this CTA's rows whose group masks are mask(g), in rounds of kListCap
-    auto run_rows = [&](auto &&mask) {
+    // attention over list positions [lo, hi): batches of 8 rows, 2 cp.async stages
+    auto gather_range = [&](int lo, int hi) {
+      const int nb = (hi - lo + kBatch - 1) / kBatch;
+      auto issue = [&](int j) {
+        uint8_t *st = ring + (j & 1) * STAGE;
+        const int rb = lo + j * kBatch;
+#pragma unroll
+        for (int m = 0; m < kBatch * CHN / 32; ++m) {
+          const int q = lane + 32 * m;
+          const int rr = q / CHN, ch = q % CHN;
+          const bool rv = rb + rr < hi;
+          const size_t off = rv ? (size_t)sh.list[rb + rr] * ROWB + (size_t)ch * 16 : 0;
+          const uint32_t dst = smem_u32(st + rr * ROWB + swz(rr, ch));
+          cp_async16(dst, kp + off, rv ? 16 : 0);
+          cp_async16(dst + kBatch * ROWB, vp + off, rv ? 16 : 0);
+        }
+      };
+      if (nb > 0) issue(0);
+      cp_async_commit();
+      for (int j = 0; j < nb; ++j) {
+        if (j + 1 < nb) issue(j + 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        compute(ring + (j & 1) * STAGE, min(kBatch, hi - (lo + j * kBatch)));
+        __syncwarp();  // stage fully read before it is refilled
+      }
+      cp_async_wait<0>();
+    };
+    auto split = [&](int n, int &lo, int &hi) {  // this warp's share of n rows (multiples of 8)
+      int per = (n + kAttWarps - 1) / kAttWarps;
+      per = (per + kBatch - 1) & ~(kBatch - 1);
+      lo = min(aw * per, n);
+      hi = min(lo + per, n);
+    };
+
+    // attention over this CTA's rows whose group masks are mask(g), in rounds of
+    // kListCap; final_sync: end with an attention-warp barrier
+    auto run_rows = [&](auto &&mask, bool final_sync) {
       const int ga = aw * 64 + lane, gb = ga + 32;  // warp aw: groups [64 aw, 64 aw + 64)
       const uint32_t ma = ga < ngrp ? mask(ga) : 0u;
       const uint32_t mb = gb < ngrp ? mask(gb) : 0u;
@@ -638,60 +732,38 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       named_sync(kBarAtt, kAttThreads);  // wtot read by all before any reuse
       for (uint32_t r0 = 0; r0 < total; r0 += kListCap) {
         // row ids of list positions [r0, r0 + kListCap)
-        auto put = [&](uint32_t pos, int t) {
-          if (pos >= r0 && pos < r0 + kListCap) {
-            const int pg = pow2 ? (t >> psh) : t / c.P;
-            const int sl = t - pg * c.P;
-            sh.list[pos - r0] =
-                ((uint32_t)__ldg(bt + pg) * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P + (uint32_t)sl;
-          }
-        };
         uint32_t pa = base + ia - ca, pb = base + ta + ib - cb;
-        for (uint32_t m = ma; m; m &= m - 1) put(pa++, t0 + ga * 32 + __ffs(m) - 1);
-        for (uint32_t m = mb; m; m &= m - 1) put(pb++, t0 + gb * 32 + __ffs(m) - 1);
+        for (uint32_t m = ma; m; m &= m - 1, ++pa)
+          if (pa >= r0 && pa < r0 + kListCap) sh.list[pa - r0] = row_of(t0 + ga * 32 + __ffs(m) - 1);
+        for (uint32_t m = mb; m; m &= m - 1, ++pb)
+          if (pb >= r0 && pb < r0 + kListCap) sh.list[pb - r0] = row_of(t0 + gb * 32 + __ffs(m) - 1);
         named_sync(kBarAtt, kAttThreads);
-        const int nl = (int)min((uint32_t)kListCap, total - r0);
-        int per = (nl + kAttWarps - 1) / kAttWarps;
-        per = (per + kBatch - 1) & ~(kBatch - 1);
-        const int lo = min(aw * per, nl), hi = min(lo + per, nl);
-        const int nb = (hi - lo + kBatch - 1) / kBatch;
-        auto issue = [&](int j) {
-          uint8_t *st = ring + (j & 1) * STAGE;
-          const int rb = lo + j * kBatch;
-#pragma unroll
-          for (int m = 0; m < kBatch * CHN / 32; ++m) {
-            const int q = lane + 32 * m;
-            const int rr = q / CHN, ch = q % CHN;
-            const bool rv = rb + rr < hi;
-            const size_t off = rv ? (size_t)sh.list[rb + rr] * ROWB + (size_t)ch * 16 : 0;
-            const uint32_t dst = smem_u32(st + rr * ROWB + swz(rr, ch));
-            cp_async16(dst, kp + off, rv ? 16 : 0);
-            cp_async16(dst + kBatch * ROWB, vp + off, rv ? 16 : 0);
-          }
-        };
-        if (nb > 0) issue(0);
-        cp_async_commit();
-        for (int j = 0; j < nb; ++j) {
-          if (j + 1 < nb) issue(j + 1);
-          cp_async_commit();
-          cp_async_wait<1>();
-          __syncwarp();
-          compute(ring + (j & 1) * STAGE, min(kBatch, hi - (lo + j * kBatch)));
-          __syncwarp();  // stage fully read before it is refilled
-        }
-        cp_async_wait<0>();
-        named_sync(kBarAtt, kAttThreads);  // list consumed before the next round
+        int lo, hi;
+        split((int)min((uint32_t)kListCap, total - r0), lo, hi);
+        gather_range(lo, hi);
+        if (final_sync || r0 + kListCap < total) named_sync(kBarAtt, kAttThreads);  // list consumed
       }
     };
 
     if (!ovf) {
-      run_rows([&](int g) { return sh.gtm[g]; });  // certainly selected: digit1 above D1
-      named_sync(kBarDone, kThreads);              // the selection tail is done
+      run_rows([&](int g) { return sh.gtm[g]; }, false);  // certainly selected: digit1 above D1
       DS_TRACE_AT(1, 4);
-      if (tail) run_rows([&](int g) { return sh.selm[g]; });
+      if (lane == 0)  // the selection warps have listed the selected candidates
+        while (*reinterpret_cast<volatile uint32_t *>(&sh.state[14]) == 0u) __nanosleep(64);
+      __syncwarp();
+      __threadfence_block();
+      const uint32_t mode = *reinterpret_cast<volatile uint32_t *>(&sh.state[14]);
+      if (mode == 1u) {  // rows at [n_gt, n_gt + n_sel): no barrier with the other warps
+        int lo, hi;
+        split((int)sh.state[13], lo, hi);
+        gather_range((int)sh.state[12] + lo, (int)sh.state[12] + hi);
+      } else if (tail) {  // did not fit behind the certain rows: a list of their own
+        named_sync(kBarAtt, kAttThreads);
+        run_rows([&](int g) { return sh.selm[g]; }, true);
+      }
     } else {  // the tail still scans the keys in this buffer: wait, then all rows
       named_sync(kBarDone, kThreads);
-      run_rows([&](int g) { return sh.gtm[g] | sh.selm[g]; });
+      run_rows([&](int g) { return sh.gtm[g] | sh.selm[g]; }, true);
     }
     DS_TRACE_AT(1, 5);
     // ---- warp partials (m, l per head; O^T fragments) -> CTA partial
