@@ -58,7 +58,7 @@ constexpr int kSh2 = 10, kD2 = 1024;  // digit 2: key bits 19..10
 constexpr int kD3 = 1024;             // digit 3: key bits 9..0
 constexpr int kCandCap = 2048;        // digit-1 boundary tokens listed
 constexpr int kMaxMembers = 512;      // 22-bit-prefix boundary tokens ranked directly
-constexpr int kListCap = 2048;        // pool rows per attention round
+constexpr int kListCap = 2048 + 64;   // pool rows per attention round (k = 2048 + batch alignment)
 constexpr int kBatch = 8;             // rows per warp batch
 constexpr int kBarAtt = 1, kBarSel = 2, kBarDone = 3, kBarRegs = 4;  // named barriers
 // register split after the common phases (64 per thread at launch):
@@ -365,7 +365,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     const int sl = t - pg * c.P;
     return ((uint32_t)__ldg(bt + pg) * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P + (uint32_t)sl;
   };
-  if (tid == 0) sh.state[14] = 0u;  // candidate rows not listed yet (read by the attention warps)
+  if (tid == 0) {
+    sh.state[14] = 0u;  // candidate rows not listed yet (read by the attention warps)
+    sh.state[15] = 0u;  // the attention warps' batch cursor
+  }
   __syncthreads();
 
   if (warp >= kAttWarps) {
@@ -543,15 +546,16 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         n_sel += x;
         n_gt += sh.cand[w].x;
       }
-      const bool fits = n_gt + n_sel <= (uint32_t)kListCap;
+      const uint32_t p0 = (n_gt + kBatch - 1) & ~(uint32_t)(kBatch - 1);  // batch-aligned start
+      const bool fits = p0 + n_sel <= (uint32_t)kListCap;
       if (fits) {
-        uint32_t pa = n_gt + base + ia - ca, pb = n_gt + base + ta + ib - cb;
+        uint32_t pa = p0 + base + ia - ca, pb = p0 + base + ta + ib - cb;
         for (uint32_t m = ma; m; m &= m - 1) sh.list[pa++] = row_of(t0 + ga * 32 + __ffs(m) - 1);
         for (uint32_t m = mb; m; m &= m - 1) sh.list[pb++] = row_of(t0 + gb * 32 + __ffs(m) - 1);
       }
       sel_sync();
       if (stid == 0) {
-        sh.state[12] = n_gt;
+        sh.state[12] = p0;
         sh.state[13] = n_sel;
         __threadfence_block();
         *reinterpret_cast<volatile uint32_t *>(&sh.state[14]) = fits ? 1u : 2u;
@@ -746,18 +750,100 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     };
 
     if (!ovf) {
-      run_rows([&](int g) { return sh.gtm[g]; }, false);  // certainly selected: digit1 above D1
+      // the certain rows (digit1 > D1) at list positions [0, n_gt)
+      const int ga = aw * 64 + lane, gb = ga + 32;  // warp aw: groups [64 aw, 64 aw + 64)
+      const uint32_t ma = ga < ngrp ? sh.gtm[ga] : 0u;
+      const uint32_t mb = gb < ngrp ? sh.gtm[gb] : 0u;
+      const uint32_t ca = __popc(ma), cb = __popc(mb);
+      uint32_t ia = ca, ib = cb;
+#pragma unroll
+      for (int o2 = 1; o2 < 32; o2 <<= 1) {
+        const uint32_t ya = __shfl_up_sync(0xffffffffu, ia, o2);
+        const uint32_t yb = __shfl_up_sync(0xffffffffu, ib, o2);
+        if (lane >= o2) {
+          ia += ya;
+          ib += yb;
+        }
+      }
+      const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31), tb = __shfl_sync(0xffffffffu, ib, 31);
+      if (lane == 0) sh.wtot[aw] = ta + tb;
+      named_sync(kBarAtt, kAttThreads);
+      uint32_t base = 0, n_gt = 0;
+      for (int w = 0; w < kAttWarps; ++w) {
+        const uint32_t x = sh.wtot[w];
+        if (w < aw) base += x;
+        n_gt += x;
+      }
+      if (n_gt <= (uint32_t)kListCap) {
+        uint32_t pa = base + ia - ca, pb = base + ta + ib - cb;
+        for (uint32_t m = ma; m; m &= m - 1) sh.list[pa++] = row_of(t0 + ga * 32 + __ffs(m) - 1);
+        for (uint32_t m = mb; m; m &= m - 1) sh.list[pb++] = row_of(t0 + gb * 32 + __ffs(m) - 1);
+        named_sync(kBarAtt, kAttThreads);  // the list of certain rows is complete
+        // batches of 8 list positions handed out by a shared cursor: batches
+        // below nb1 are certain rows; the selected candidates follow from
+        // position 8 * nb1 once the selection warps raise the flag
+        const int nb1 = ((int)n_gt + kBatch - 1) / kBatch;
+        auto grab = [&](int &nvalid) -> int {  // next batch (or -1) and its valid rows
+          int j = 0, nv = 0;
+          if (lane == 0) {
+            j = (int)atomicAdd(&sh.state[15], 1u);
+            if (j < nb1) {
+              nv = min(kBatch, (int)n_gt - j * kBatch);
+            } else {
+              uint32_t f;
+              while ((f = *reinterpret_cast<volatile uint32_t *>(&sh.state[14])) == 0u) __nanosleep(64);
+              __threadfence_block();
+              const int lim = (int)sh.state[12] + (int)sh.state[13];
+              if (f != 1u || j * kBatch >= lim) j = -1;
+              else nv = min(kBatch, lim - j * kBatch);
+            }
+          }
+          nvalid = __shfl_sync(0xffffffffu, nv, 0);
+          return __shfl_sync(0xffffffffu, j, 0);
+        };
+        auto issue = [&](int j, int nv, int stg) {
+          uint8_t *st = ring + stg * STAGE;
+          const int rb = j * kBatch;
+#pragma unroll
+          for (int m = 0; m < kBatch * CHN / 32; ++m) {
+            const int q = lane + 32 * m;
+            const int rr = q / CHN, ch = q % CHN;
+            const bool rv = rr < nv;
+            const size_t off = rv ? (size_t)sh.list[rb + rr] * ROWB + (size_t)ch * 16 : 0;
+            const uint32_t dst = smem_u32(st + rr * ROWB + swz(rr, ch));
+            cp_async16(dst, kp + off, rv ? 16 : 0);
+            cp_async16(dst + kBatch * ROWB, vp + off, rv ? 16 : 0);
+          }
+        };
+        int nv_cur = 0, stg = 0;
+        int cur = grab(nv_cur);
+        if (cur >= 0) issue(cur, nv_cur, 0);
+        cp_async_commit();
+        while (cur >= 0) {
+          int nv_nxt = 0;
+          const int nxt = grab(nv_nxt);
+          if (nxt >= 0) issue(nxt, nv_nxt, stg ^ 1);
+          cp_async_commit();
+          cp_async_wait<1>();
+          __syncwarp();
+          compute(ring + stg * STAGE, nv_cur);
+          __syncwarp();  // stage fully read before it is refilled
+          cur = nxt;
+          nv_cur = nv_nxt;
+          stg ^= 1;
+        }
+        cp_async_wait<0>();
+      } else {  // more certain rows than one list: rounds
+        named_sync(kBarAtt, kAttThreads);
+        run_rows([&](int g) { return sh.gtm[g]; }, false);
+      }
       DS_TRACE_AT(1, 4);
-      if (lane == 0)  // the selection warps have listed the selected candidates
+      if (lane == 0)  // (the flag: set by now in the cursor path)
         while (*reinterpret_cast<volatile uint32_t *>(&sh.state[14]) == 0u) __nanosleep(64);
       __syncwarp();
       __threadfence_block();
-      const uint32_t mode = *reinterpret_cast<volatile uint32_t *>(&sh.state[14]);
-      if (mode == 1u) {  // rows at [n_gt, n_gt + n_sel): no barrier with the other warps
-        int lo, hi;
-        split((int)sh.state[13], lo, hi);
-        gather_range((int)sh.state[12] + lo, (int)sh.state[12] + hi);
-      } else if (tail) {  // did not fit behind the certain rows: a list of their own
+      if (*reinterpret_cast<volatile uint32_t *>(&sh.state[14]) != 1u && tail) {
+        // the candidates did not fit behind the certain rows: a list of their own
         named_sync(kBarAtt, kAttThreads);
         run_rows([&](int g) { return sh.selm[g]; }, true);
       }
