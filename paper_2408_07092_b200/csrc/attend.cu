@@ -588,7 +588,12 @@ __global__ void __launch_bounds__(kMmaThreads, 1) attn_mma_kernel(AttnParams p) 
         o[nd][1] *= alpha;
       }
       // ---- O += P V
-      const uint32_t pa[4] = {pack2<T>(pv[0][0], pv[0][1]), 0u, pack2<T>(pv[1][0], pv[1][1]), 0u};
+      // P as hi + lo 16-bit pairs (see decode.cu): ~16 significant bits in PV
+      const uint32_t ph0 = pack2<T>(pv[0][0], pv[0][1]), ph1 = pack2<T>(pv[1][0], pv[1][1]);
+      const float2 f0 = Elem<T>::unpack2(ph0), f1 = Elem<T>::unpack2(ph1);
+      const uint32_t pa[4] = {ph0, 0u, ph1, 0u};
+      const uint32_t pl[4] = {pack2<T>(pv[0][0] - f0.x, pv[0][1] - f0.y), 0u,
+                              pack2<T>(pv[1][0] - f1.x, pv[1][1] - f1.y), 0u};
       {
         const int mi = lane >> 3;
         const int vrow = (mi & 1) * 8 + (lane & 7);
@@ -599,6 +604,8 @@ __global__ void __launch_bounds__(kMmaThreads, 1) attn_mma_kernel(AttnParams p) 
           ldmatrix_x4_trans(vaddr + nd2 * 32, v0, v1, v2, v3);
           Mma<T>::run(o[2 * nd2], pa, v0, v1);
           Mma<T>::run(o[2 * nd2 + 1], pa, v2, v3);
+          Mma<T>::run(o[2 * nd2], pl, v0, v1);
+          Mma<T>::run(o[2 * nd2 + 1], pl, v2, v3);
         }
       }
       __syncwarp();  // every lane is done with this stage before it is refilled

@@ -660,7 +660,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         o[mt][2] *= alo;
         o[mt][3] *= ahi;
       }
+      // P as a hi + lo pair of 16-bit values (hi = RNE(p), lo = RNE(p - hi)):
+      // ~16 significant bits, so the PV product is not limited by the 8-bit
+      // bf16 mantissa (R14 holds for peaked softmaxes too)
       const uint32_t bp = pack2<T>(p0, p1);
+      const float2 ph = Elem<T>::unpack2(bp);
+      const uint32_t bl = pack2<T>(p0 - ph.x, p1 - ph.y);
       const uint32_t vb = smem_u32(st + kBatch * ROWB) + (lane & 7) * ROWB;
 #pragma unroll
       for (int j = 0; j < NKS / 2; ++j) {
@@ -668,6 +673,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         ldmatrix_x4_trans(vb + swz(lane, 4 * j + (lane >> 3)), v0, v1, v2, v3);
         Mma8<T>::run(o[2 * j], v0, v1, bp);
         Mma8<T>::run(o[2 * j + 1], v2, v3, bp);
+        Mma8<T>::run(o[2 * j], v0, v1, bl);
+        Mma8<T>::run(o[2 * j + 1], v2, v3, bl);
       }
     };
 
