@@ -50,9 +50,12 @@ def lib():
         L.oracle_argtopk.restype = i
         L.oracle_attend.argtypes = [P, P, P, i, P, i, P]
         L.oracle_dense_attention.argtypes = [P, P, P, i, i, P]
-        L.oracle_ds_decode_unit.argtypes = [P, P, i, P, P, P, P, i, i, i, i, P, P, P, P]
+        L.oracle_quantize_label_4bit.argtypes = [P, i, i, i, P, P]
+        L.oracle_pack_int4.argtypes = [P, i, i, P]
+        L.oracle_approx_scores_q4.argtypes = [P, P, P, i, i, P]
+        L.oracle_ds_decode_unit.argtypes = [P, P, i, P, P, P, P, P, P, i, i, i, i, P, P, P, P]
         L.oracle_ds_decode_unit.restype = i
-        L.oracle_decode_batch.argtypes = [P, P, P, P, P, P, P, i, i, i, i, i, i, i, i, P, P, i]
+        L.oracle_decode_batch.argtypes = [P, P, P, P, P, P, P, P, P, i, i, i, i, i, i, i, i, P, P, i]
         L.oracle_decode_batch.restype = i
         L.oracle_calibrate.argtypes = [P, P, i, i, i, i, i, i, ctypes.c_uint64, P, P]
         L.oracle_calibrate.restype = i
@@ -100,6 +103,39 @@ def approx_scores(qlab, L):
     return out
 
 
+SCALE_FP16, SCALE_BF16, SCALE_FP32 = 0, 1, 2   # the ds_dtype numbering
+SCALE_DTYPE = {"fp16": SCALE_FP16, "bf16": SCALE_BF16, "fp32": SCALE_FP32}
+
+
+def quantize_label_4bit(L, scale_dtype):
+    """f2 (reading R16): L [S][r] -> (codes int8 [S][r] in [-7, 7], scale fp32 [S])."""
+    L = _f32(L)
+    S, r = L.shape
+    codes = np.empty((S, r), np.int8)
+    scale = np.empty(S, np.float32)
+    lib().oracle_quantize_label_4bit(_p(L), S, r, SCALE_DTYPE.get(scale_dtype, scale_dtype), _p(codes),
+                                     _p(scale))
+    return codes, scale
+
+
+def pack_int4(codes):
+    """The stored code bytes [S][ceil(r/2)]: code 2i low nibble, 2i+1 high nibble."""
+    codes = np.ascontiguousarray(codes, dtype=np.int8)
+    S, r = codes.shape
+    out = np.empty((S, (r + 1) // 2), np.uint8)
+    lib().oracle_pack_int4(_p(codes), S, r, _p(out))
+    return out
+
+
+def approx_scores_q4(qlab, codes, scale):
+    """a2 over a 4-bit label: s_hat[t] = (fma-chain_j qlab[j]*c[t][j]) * scale[t]."""
+    qlab, scale = _f32(qlab), _f32(scale)
+    codes = np.ascontiguousarray(codes, dtype=np.int8)
+    out = np.empty(codes.shape[0], np.float32)
+    lib().oracle_approx_scores_q4(_p(qlab), _p(codes), _p(scale), codes.shape[0], codes.shape[1], _p(out))
+    return out
+
+
 def argtopk(scores, k):
     """a3: ascending indices of the k largest scores, ties -> lower index. Returns (idx, tau)."""
     s = _f32(scores)
@@ -124,8 +160,9 @@ def dense_attention(q, K, V):
     return y
 
 
-def ds_decode_unit(q, K, V, L, C, k, q_sel=None):
-    """Algorithm 1 for one unit. q [G][d]. Returns (y [G][d], idx, shat, tau)."""
+def ds_decode_unit(q, K, V, L, C, k, q_sel=None, codes=None, scale=None):
+    """Algorithm 1 for one unit. q [G][d]. Returns (y [G][d], idx, shat, tau).
+    codes/scale (from quantize_label_4bit): line 2 over the 4-bit label."""
     q = _f32(q)
     if q.ndim == 1:
         q = q[None]
@@ -137,14 +174,18 @@ def ds_decode_unit(q, K, V, L, C, k, q_sel=None):
     idx = np.empty(max(1, min(k, S)), np.int32)
     shat = np.empty(max(1, S), np.float32)
     tau = np.zeros(1, np.float32)
-    n = lib().oracle_ds_decode_unit(_p(q), _p(qs), G, _p(K), _p(V), _p(L), _p(C), S, d,
-                                    L.shape[1], k, _p(y), _p(idx), _p(shat), _p(tau))
+    if scale is not None:
+        codes = np.ascontiguousarray(codes, dtype=np.int8)
+        scale = _f32(scale)
+    n = lib().oracle_ds_decode_unit(_p(q), _p(qs), G, _p(K), _p(V), _p(L), _p(codes), _p(scale), _p(C), S,
+                                    d, L.shape[1], k, _p(y), _p(idx), _p(shat), _p(tau))
     return y, idx[:n], shat[:S], float(tau[0])
 
 
-def decode_batch(q, K, V, L, C, seq_lens, k, mode=0, q_sel=None, nthreads=1):
+def decode_batch(q, K, V, L, C, seq_lens, k, mode=0, q_sel=None, nthreads=1, codes=None, scale=None):
     """Batched oracle. q [B][Hq][d]; K,V [B][Hkv][Smax][d]; L [B][Hkv][Smax][r];
-    C [Hkv][r]; seq_lens [B]. mode 0 = DS (Alg. 1), 1 = dense. Returns (y, idx)."""
+    C [Hkv][r]; seq_lens [B]. mode 0 = DS (Alg. 1), 1 = dense. Returns (y, idx).
+    codes [B][Hkv][Smax][r] + scale [B][Hkv][Smax]: score over the 4-bit label."""
     q, K, V = _f32(q), _f32(K), _f32(V)
     B, Hq, d = q.shape
     Hkv, Smax = K.shape[1], K.shape[2]
@@ -155,7 +196,11 @@ def decode_batch(q, K, V, L, C, seq_lens, k, mode=0, q_sel=None, nthreads=1):
     qs = _f32(q_sel) if q_sel is not None else None
     y = np.zeros((B, Hq, d), np.float32)
     idx = np.full((B, Hkv, max(k, 1)), -1, np.int32)
-    rc = lib().oracle_decode_batch(_p(q), _p(qs), _p(K), _p(V), _p(Lp), _p(C), _p(seq), B, Hq, Hkv,
+    if scale is not None:
+        codes = np.ascontiguousarray(codes, dtype=np.int8)
+        scale = _f32(scale)
+    rc = lib().oracle_decode_batch(_p(q), _p(qs), _p(K), _p(V), _p(Lp), _p(codes), _p(scale), _p(C), _p(seq),
+                                   B, Hq, Hkv,
                                    Smax, d, r, k, mode, _p(y), _p(idx) if mode == 0 else None,
                                    nthreads)
     if rc != 0:

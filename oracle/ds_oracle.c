@@ -10,7 +10,7 @@
  *
  * Every function below follows a passage of /root/reference/PAPER.md
  * ("P:n" = line n) in the paper's order and notation; where the paper is
- * silent the DESIGN.md reading it takes is named (R1..R15, which mirror
+ * silent the DESIGN.md reading it takes is named (R1..R16, which extend
  * SURVEY.md 8(c)).  Floating point is fp32 as BASELINE.json's north_star
  * fixes ("a plain, slow CPU oracle in fp32"); calibration statistics are
  * accumulated in fp64.  No blocking, fusion or reordering beyond what the
@@ -62,6 +62,74 @@ void oracle_approx_scores(const float *qlab, const float *L, int S, int r,
     float s = 0.0f;
     for (int j = 0; j < r; ++j) s = fmaf(qlab[j], L[(size_t)t * r + j], s);
     shat[t] = s;
+  }
+}
+
+/* f2  4-bit label cache ("Since approximate attention is not
+ *     sensitive to precision, we can store the label cache in 4-bit").
+ *     The paper names no scheme; reading R16 (symmetric
+ *     per-row quantisation, codes in [-7, 7]) with the scale stored in the
+ *     cache's own element type:
+ *       a    = max_j |L[t][j]|
+ *       s32  = a / 7 in fp32 (1 when a == 0)
+ *       s    = s32 rounded to nearest-even in the scale type (fp16 / bf16 /
+ *              fp32: scale_dtype 0 / 1 / 2, the ds_dtype numbering), then
+ *              widened; s = 1 if that rounding gives 0
+ *       c_j  = clamp(round_half_away_from_zero(L[t][j] / s), -7, 7), the
+ *              quotient in fp32
+ *     The dequantised label value is c_j * s.                            */
+static float oracle_round_to_dtype(float x, int scale_dtype) {
+  if (scale_dtype == 0) return (float)(_Float16)x; /* IEEE binary16, RNE */
+  if (scale_dtype == 1) return (float)(__bf16)x;   /* bfloat16, RNE */
+  return x;
+}
+
+void oracle_quantize_label_4bit(const float *L /*[S][r]*/, int S, int r,
+                                int scale_dtype, int8_t *codes /*[S][r]*/,
+                                float *scale /*[S]*/) {
+  for (int t = 0; t < S; ++t) {
+    const float *row = L + (size_t)t * r;
+    float a = 0.0f;
+    for (int j = 0; j < r; ++j)
+      if (fabsf(row[j]) > a) a = fabsf(row[j]);
+    float s32 = a == 0.0f ? 1.0f : a / 7.0f;
+    float s = oracle_round_to_dtype(s32, scale_dtype);
+    if (s == 0.0f) s = 1.0f;
+    for (int j = 0; j < r; ++j) {
+      float v = row[j] / s;
+      double c = v < 0.0f ? -floor(-(double)v + 0.5) : floor((double)v + 0.5);
+      if (c > 7.0) c = 7.0;
+      if (c < -7.0) c = -7.0;
+      codes[(size_t)t * r + j] = (int8_t)c;
+    }
+    scale[t] = s;
+  }
+}
+
+/* The stored code layout (reading R16, SPEC int4 packing): row t holds
+ * ceil(r/2) bytes; byte i carries code 2i in its low nibble and code
+ * 2i+1 in its high nibble, each as a 4-bit two's complement number; an
+ * odd r leaves the last high nibble 0.                                  */
+void oracle_pack_int4(const int8_t *codes, int S, int r, uint8_t *out) {
+  int rb = (r + 1) / 2;
+  for (int t = 0; t < S; ++t)
+    for (int i = 0; i < rb; ++i) {
+      int lo = codes[(size_t)t * r + 2 * i];
+      int hi = 2 * i + 1 < r ? codes[(size_t)t * r + 2 * i + 1] : 0;
+      out[(size_t)t * rb + i] = (uint8_t)((lo & 15) | ((hi & 15) << 4));
+    }
+}
+
+/* a2 over a 4-bit label (reading R16): the fp32 fma chain over j of
+ * q_label[j] * c_j (exact small integers), then one multiply by the
+ * row's scale:  s_hat[t] = (fma-chain_j qlab[j] * c_j) * s_t.  Up to
+ * rounding this is q_label . (c * s), the dequantised label.            */
+void oracle_approx_scores_q4(const float *qlab, const int8_t *codes,
+                             const float *scale, int S, int r, float *shat) {
+  for (int t = 0; t < S; ++t) {
+    float acc = 0.0f;
+    for (int j = 0; j < r; ++j) acc = fmaf(qlab[j], (float)codes[(size_t)t * r + j], acc);
+    shat[t] = acc * scale[t];
   }
 }
 
@@ -153,9 +221,12 @@ void oracle_dense_attention(const float *q, const float *K, const float *V,
  *                  q_attn for Double Sparsity, the predicted next-layer
  *                  query for Double Sparsity-Offload.
  *   K, V   [S][d], L [S][r], C [r].
+ *   codes [S][r], scale [S]: a 4-bit label (reading R16) used for line 2
+ *                  instead of L when scale is not NULL.
  * Outputs y [G][d]; optional idx [k_eff], shat [S], tau.               */
 int oracle_ds_decode_unit(const float *q_attn, const float *q_sel, int G,
                           const float *K, const float *V, const float *L,
+                          const int8_t *codes, const float *scale,
                           const int32_t *C, int S, int d, int r, int k,
                           float *y, int32_t *idx_out, float *shat_out,
                           float *tau_out) {
@@ -163,7 +234,10 @@ int oracle_ds_decode_unit(const float *q_attn, const float *q_sel, int G,
   float *shat = (float *)malloc(sizeof(float) * (size_t)(S > 0 ? S : 1));
   int32_t *idx = (int32_t *)malloc(sizeof(int32_t) * (size_t)(S > 0 ? S : 1));
   oracle_query_label(q_sel, G, d, C, r, qlab);              /* line 1 */
-  oracle_approx_scores(qlab, L, S, r, shat);                /* line 2 */
+  if (scale)                                                /* line 2 */
+    oracle_approx_scores_q4(qlab, codes, scale, S, r, shat);   /* 4-bit label (R16) */
+  else
+    oracle_approx_scores(qlab, L, S, r, shat);
   float tau = 0.0f;
   int keff = oracle_argtopk(shat, S, k, idx, &tau);         /* line 3 */
   for (int g = 0; g < G; ++g)                               /* lines 4-5 */
@@ -182,10 +256,13 @@ int oracle_ds_decode_unit(const float *q_attn, const float *q_sel, int G,
  *   q [B][Hq][d], K,V [B][Hkv][Smax][d], L [B][Hkv][Smax][r],
  *   C [Hkv][r], seq_lens [B]; y [B][Hq][d]; idx [B][Hkv][k] (-1 padded).
  * mode 0 = Double Sparsity (Alg. 1), mode 1 = dense attention.
+ * codes [B][Hkv][Smax][r] + scale [B][Hkv][Smax] (nullable): 4-bit label.
  * nthreads > 1 statically partitions the independent units over pthreads
  * (the per-unit code is unchanged); it exists only for the cpu_baseline. */
 typedef struct {
   const float *q, *qsel, *K, *V, *L;
+  const int8_t *codes;
+  const float *scale;
   const int32_t *C, *seq_lens;
   int B, Hq, Hkv, Smax, d, r, k, mode;
   float *y;
@@ -210,7 +287,10 @@ static void *oracle_run_units(void *arg) {
     } else {
       int32_t *idx = j->idx ? j->idx + ((size_t)b * j->Hkv + h) * j->k : NULL;
       int keff = oracle_ds_decode_unit(q, qs, G, j->K + kv * j->d, j->V + kv * j->d,
-                                       j->L + kv * j->r, j->C + (size_t)h * j->r, S,
+                                       j->L + kv * j->r,
+                                       j->codes ? j->codes + kv * j->r : NULL,
+                                       j->scale ? j->scale + kv : NULL,
+                                       j->C + (size_t)h * j->r, S,
                                        j->d, j->r, j->k, y, idx, NULL, NULL);
       if (idx)
         for (int i = keff; i < j->k; ++i) idx[i] = -1;
@@ -220,7 +300,8 @@ static void *oracle_run_units(void *arg) {
 }
 
 int oracle_decode_batch(const float *q, const float *qsel, const float *K,
-                        const float *V, const float *L, const int32_t *C,
+                        const float *V, const float *L, const int8_t *codes,
+                        const float *scale, const int32_t *C,
                         const int32_t *seq_lens, int B, int Hq, int Hkv,
                         int Smax, int d, int r, int k, int mode, float *y,
                         int32_t *idx, int nthreads) {
@@ -231,7 +312,7 @@ int oracle_decode_batch(const float *q, const float *qsel, const float *K,
   oracle_job *jobs = (oracle_job *)calloc((size_t)nthreads, sizeof(oracle_job));
   pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
   for (int i = 0; i < nthreads; ++i) {
-    oracle_job j = {q, qsel ? qsel : q, K, V, L, C, seq_lens, B, Hq, Hkv,
+    oracle_job j = {q, qsel ? qsel : q, K, V, L, codes, scale, C, seq_lens, B, Hq, Hkv,
                     Smax, d, r, k, mode, y, idx,
                     (int)((long)units * i / nthreads),
                     (int)((long)units * (i + 1) / nthreads)};
