@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--structure", default="iid", choices=["iid", "clustered"])
+    ap.add_argument("--label", default="native", choices=["native", "int4"],
+                    help="label cache storage: K's dtype (north_star's byte model) or 4-bit (P:171, f2)")
     ap.add_argument("--mode", default="weak", choices=["weak", "allgather"])
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -200,7 +202,7 @@ class Clocks:
 
 
 # ----------------------------------------------------------- our GPU arm
-def build_layers(cfg, L, rank, structure, device):
+def build_layers(cfg, L, rank, structure, device, label="native"):
     import paper_2408_07092_b200 as ds
     layers = []
     for l in range(L):
@@ -210,7 +212,7 @@ def build_layers(cfg, L, rank, structure, device):
         C = ds.ds_calibrate_channels(Qc, Kc, cfg.Hkv, cfg.r)            # offline, untimed
         cache = ds.LayerCache.allocate(cfg.B, cfg.Hq, cfg.Hkv, cfg.d, cfg.S, cfg.r, synth.DTYPES[cfg.dtype],
                                        lay.block_table, num_pages=lay.num_pages, page_size=cfg.page_size,
-                                       device=device, channel_idx=C)
+                                       device=device, channel_idx=C, label_format=label)
         ds.prefill(cache, lay.K, lay.V, lay.seq_lens)
         # the decode step's inputs: the current token (position S-1) and its query
         k_new = lay.K[:, :, cfg.S - 1:cfg.S].transpose(1, 2).contiguous()
@@ -263,7 +265,7 @@ def run_ours(args, dist):
     cfg, h0 = shard_plan(full, dist.world, dist.rank, args.mode)
     L = args.layers
     hbm_peak, peak_src = peaks()
-    layers = build_layers(cfg, L, dist.rank if args.mode == "weak" else 0, args.structure, dev)
+    layers = build_layers(cfg, L, dist.rank if args.mode == "weak" else 0, args.structure, dev, args.label)
     k = cfg.k
     ws = ds.workspace(ds.ds_decode_workspace_size(layers[0]["cache"], k), dev)
     stream = torch.cuda.Stream(dev)
@@ -300,10 +302,10 @@ def run_ours(args, dist):
     ms_dec_total, _ = time_graph(decode_only, args.steps, 2, dist, stream)
     us_decode = ms_dec_total / args.steps / L * 1000.0
 
-    bytes_layer = ledger.layer_bytes_alg(cfg)
+    bytes_layer = ledger.layer_bytes_alg(cfg, args.label)
     n_ranks = dist.world
     total_bytes = bytes_layer * L * (n_ranks if args.mode == "weak" else 1) if args.mode == "weak" else \
-        ledger.layer_bytes_alg(full) * L
+        ledger.layer_bytes_alg(full, args.label) * L
     value = total_bytes / (ms_step / 1e3) / 1e9
     us_layer = ms_step * 1000.0 / L
     res = {
@@ -312,7 +314,8 @@ def run_ours(args, dist):
         "scaling": "weak" if args.mode == "weak" else "strong", "vs_baseline": None, "dtype": cfg.dtype,
         "data": "synthetic (seeded N(0,1) q/K/V, 8 planted outlier channels per KV head, random page order)",
         "config": {"workload": f"{full.name}: B={full.B} Hq={full.Hq} Hkv={full.Hkv} d={full.d} S={full.S} "
-                               f"r={full.r} k={full.k} {full.dtype}", "layers_resident": L,
+                               f"r={full.r} k={full.k} {full.dtype}" + (" label=int4" if args.label == "int4" else ""),
+                   "label": args.label, "layers_resident": L,
                    "structure": args.structure, "page_size": cfg.page_size,
                    "parallelism": (f"dp{n_ranks}" if args.mode == "weak" else f"kv-head-shard{n_ranks}+allgather"),
                    "l2": f"inputs > L2: each step touches {L} x {bytes_layer / 2**20:.0f} MiB of distinct layer caches"},
@@ -323,7 +326,7 @@ def run_ours(args, dist):
     achieved = bytes_layer / (us_decode * 1e-6) / 1e9
     n_dec = ds.ds_decode_launches(layers[0]["cache"], cfg.k)
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"traffic_{full.name}.json")
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{full.name}" + ("_int4" if args.label == "int4" else "") + ".json")
     if os.path.exists(tpath):
         try:
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch_group")
@@ -352,7 +355,7 @@ def run_ours(args, dist):
         res["dense_us_per_layer"] = round(us_dense, 3)
         res["dense_gbs"] = round(ledger.layer_bytes_dense(cfg) / (us_dense * 1e-6) / 1e9, 1)
         res["speedup_vs_dense"] = round(us_dense / us_decode, 3)
-        res["byte_ratio_ceiling"] = round(ledger.byte_ratio_ceiling(cfg), 3)
+        res["byte_ratio_ceiling"] = round(ledger.byte_ratio_ceiling(cfg, args.label), 3)
         del dws
 
     if not args.no_e2e:
@@ -362,7 +365,7 @@ def run_ours(args, dist):
     del layers
     torch.cuda.empty_cache()
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
-        res["cpu_baseline"] = cpu_baseline(full, budget_s=12.0)
+        res["cpu_baseline"] = cpu_baseline(full, budget_s=12.0, label=args.label)
     return res
 
 
@@ -403,8 +406,8 @@ def e2e(args, dist, layers, ws, k, stream, cfg):
     ms = dist.max(e0.elapsed_time(e1) / args.steps)
     L = len(layers)
     nr = dist.world if args.mode == "weak" else 1
-    val = ledger.layer_bytes_alg(cfg) * L * nr / (ms / 1e3) / 1e9 if args.mode == "weak" else \
-        ledger.layer_bytes_alg(synth.CONFIGS[args.config]) * L / (ms / 1e3) / 1e9
+    val = ledger.layer_bytes_alg(cfg, args.label) * L * nr / (ms / 1e3) / 1e9 if args.mode == "weak" else \
+        ledger.layer_bytes_alg(synth.CONFIGS[args.config], args.label) * L / (ms / 1e3) / 1e9
     return {"value": round(val, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": round(ms, 5), "api": "paper_2408_07092_b200.ds_append_kv + ds_decode_attention (eager)"}
 
@@ -449,8 +452,9 @@ def extra_configs(args):
 
 
 # ------------------------------------------------------ the oracle (CPU)
-def oracle_sample(cfg: synth.Config, n_seq: int, seed: int):
-    """Host inputs for n_seq sequences of cfg (all H_kv units each)."""
+def oracle_sample(cfg: synth.Config, n_seq: int, seed: int, label="native"):
+    """Host inputs for n_seq sequences of cfg (all H_kv units each); with
+    label="int4" also the oracle's 4-bit codes and scales of the label."""
     import oracle
     sc = cfg.with_(B=n_seq)
     lay = synth.make_layer(sc, seed, device="cpu")
@@ -458,31 +462,36 @@ def oracle_sample(cfg: synth.Config, n_seq: int, seed: int):
     C = lay.C_plant.numpy()
     import numpy as np
     L = np.empty((sc.B, sc.Hkv, sc.S, sc.r), np.float32)
+    q4 = None
+    if label == "int4":
+        q4 = dict(codes=np.empty((sc.B, sc.Hkv, sc.S, sc.r), np.int8), scale=np.empty((sc.B, sc.Hkv, sc.S), np.float32))
     for b in range(sc.B):
         for h in range(sc.Hkv):
             L[b, h] = oracle.label_gather(K[b, h], C[h])
-    return sc, q, K, V, L, C, lay.seq_lens.numpy()
+            if q4 is not None:
+                q4["codes"][b, h], q4["scale"][b, h] = oracle.quantize_label_4bit(L[b, h], cfg.dtype)
+    return sc, q, K, V, L, C, lay.seq_lens.numpy(), (q4 or {})
 
 
-def cpu_baseline(cfg: synth.Config, budget_s: float = 12.0, nthreads=None):
+def cpu_baseline(cfg: synth.Config, budget_s: float = 12.0, nthreads=None, label="native"):
     """The oracle as it stands, on this host's cores, on a bounded sample of the
     same workload: whole sequences (all KV heads) of cfg, as many as fit the
     time budget (pilot-timed)."""
     import oracle
     nthreads = nthreads or os.cpu_count() or 1
     n_seq = max(1, -(-nthreads // cfg.Hkv))            # enough units to occupy every core
-    sc, q, K, V, L, C, sl = oracle_sample(cfg, n_seq, seed=cfg.seed_base + 777)
+    sc, q, K, V, L, C, sl, q4 = oracle_sample(cfg, n_seq, seed=cfg.seed_base + 777, label=label)
     nthreads = min(nthreads, sc.units)
     t = time.perf_counter()
-    oracle.decode_batch(q, K, V, L, C, sl, cfg.k, nthreads=nthreads)
+    oracle.decode_batch(q, K, V, L, C, sl, cfg.k, nthreads=nthreads, **q4)
     pilot = time.perf_counter() - t
     reps = max(1, int(budget_s / max(pilot, 1e-3)))
     t = time.perf_counter()
     for _ in range(reps):
-        oracle.decode_batch(q, K, V, L, C, sl, cfg.k, nthreads=nthreads)
+        oracle.decode_batch(q, K, V, L, C, sl, cfg.k, nthreads=nthreads, **q4)
     dt = time.perf_counter() - t
     units = sc.units * reps
-    bytes_ = units * ledger.unit_bytes_alg(cfg.S, cfg.d, cfg.r, cfg.k, cfg.elem)
+    bytes_ = units * ledger.unit_bytes_alg(cfg.S, cfg.d, cfg.r, cfg.k, cfg.elem, label)
     return {"value": round(bytes_ / dt / 1e9, 4), "unit": "GB/s", "cores": nthreads, "kind": "oracle",
             "sample": f"{reps} x {sc.B} sequences ({sc.units} units of {cfg.name}, S={cfg.S}, k={cfg.k}), "
                       f"Algorithm 1 in plain fp32 C, {dt:.1f} s",
@@ -494,22 +503,22 @@ def run_reference(args, dist):
     full = synth.CONFIGS[args.config]
     nthreads = os.cpu_count() or 1
     n_seq = max(1, -(-nthreads // full.Hkv))
-    sc, q, K, V, L, C, sl = oracle_sample(full, n_seq, seed=full.seed_base + 777)
+    sc, q, K, V, L, C, sl, q4 = oracle_sample(full, n_seq, seed=full.seed_base + 777, label=args.label)
     nthreads = min(nthreads, sc.units)
     t = time.perf_counter()
-    oracle.decode_batch(q, K, V, L, C, sl, full.k, nthreads=nthreads)
+    oracle.decode_batch(q, K, V, L, C, sl, full.k, nthreads=nthreads, **q4)
     pilot = time.perf_counter() - t
     reps = max(1, int(2.0 / max(pilot, 1e-3)))     # ~2 s of CPU work per step
     for _ in range(args.warmup):
         for _ in range(reps):
-            oracle.decode_batch(q, K, V, L, C, sl, full.k, nthreads=nthreads)
+            oracle.decode_batch(q, K, V, L, C, sl, full.k, nthreads=nthreads, **q4)
     t = time.perf_counter()
     for _ in range(args.steps):
         for _ in range(reps):
-            oracle.decode_batch(q, K, V, L, C, sl, full.k, nthreads=nthreads)
+            oracle.decode_batch(q, K, V, L, C, sl, full.k, nthreads=nthreads, **q4)
     dt = time.perf_counter() - t
     units = sc.units * reps * args.steps
-    value = units * ledger.unit_bytes_alg(full.S, full.d, full.r, full.k, full.elem) / dt / 1e9
+    value = units * ledger.unit_bytes_alg(full.S, full.d, full.r, full.k, full.elem, args.label) / dt / 1e9
     ms_step = dt / args.steps * 1e3
     sample = f"{reps} x {sc.B} sequences ({sc.units} units) of {full.name} per step, plain fp32 C oracle"
     return {"metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
@@ -517,7 +526,8 @@ def run_reference(args, dist):
             "scaling": "weak", "vs_baseline": None, "dtype": full.dtype, "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"{full.name}: B={full.B} Hq={full.Hq} Hkv={full.Hkv} d={full.d} S={full.S} "
-                                   f"r={full.r} k={full.k} {full.dtype}", "sample_per_step": sample},
+                                   f"r={full.r} k={full.k} {full.dtype}" + (" label=int4" if args.label == "int4" else ""),
+                       "label": args.label, "sample_per_step": sample},
             "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": nthreads, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

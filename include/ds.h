@@ -27,8 +27,9 @@
  *    append positions in range, finite inputs) are the caller's contract
  *    and are not checked: violating them is undefined behaviour.
  *  - dtype: q, K, V, the label cache and out share one element type.  The
- *    label cache has the same 16-bit (or 32-bit) type as K, so
- *    "label == channel gather of K" holds bit for bit (DESIGN reading R8).
+ *    default (DS_LABEL_NATIVE) label cache has the same 16-bit (or 32-bit)
+ *    type as K, so "label == channel gather of K" holds bit for bit (DESIGN
+ *    reading R8).  DS_LABEL_INT4 stores it in 4 bits (reading R16).
  *  - Supported shapes: head_dim in {64, 128}; G = num_q_heads /
  *    num_kv_heads in {1, 2, 4, 8}; 1 <= r <= head_dim; page_size >= 1.
  *    Others return DS_ERR_UNSUPPORTED.
@@ -55,6 +56,24 @@ typedef enum {
 
 typedef enum { DS_FP16 = 0, DS_BF16 = 1, DS_FP32 = 2 } ds_dtype;
 
+/* Label-cache storage ("Since approximate attention is not
+ * sensitive to precision, we can store the label cache in 4-bit"):
+ *   DS_LABEL_NATIVE: label [batch][num_kv_heads][max_seq_len][r] of dtype,
+ *                    a bit copy of K's r channels (reading R8).
+ *   DS_LABEL_INT4  : reading R16, symmetric per-token quantisation.  For
+ *                    the r channel values x_j of a token:
+ *                      s   = RNE_dtype(max_j |x_j| / 7)  (fp32 divide; 1 if
+ *                            max is 0 or the rounding gives 0)
+ *                      c_j = clamp(round_half_away(x_j / s), -7, 7)
+ *                    label       : uint8 [batch][num_kv_heads][max_seq_len][ceil(r/2)],
+ *                                  byte i = c_{2i} (low nibble) | c_{2i+1} << 4,
+ *                                  4-bit two's complement, an odd r pads 0;
+ *                    label_scale : dtype [batch][num_kv_heads][max_seq_len] = s.
+ *                    Line 2 becomes s_hat[t] = (fp32 fma chain over j of
+ *                    q_label[j] * c_j) * s_t.  Per token ceil(r/2) + e bytes
+ *                    instead of r * e (6 instead of 16 at r = 8, 16-bit). */
+typedef enum { DS_LABEL_NATIVE = 0, DS_LABEL_INT4 = 1 } ds_label_format;
+
 /* Outlier-channel modes of Table 3: qk (default), q, k, random. */
 typedef enum { DS_CALIB_QK = 0, DS_CALIB_Q = 1, DS_CALIB_K = 2, DS_CALIB_RANDOM = 3 } ds_calib_mode;
 
@@ -67,7 +86,12 @@ typedef enum { DS_CALIB_QK = 0, DS_CALIB_Q = 1, DS_CALIB_K = 2, DS_CALIB_RANDOM 
  *   seq_lens       : int32 [batch]; attention reads tokens t < seq_lens[b]
  *                    (the caller appends the current token first, reading R10)
  *   label          : [batch][num_kv_heads][max_seq_len][r]   K_label
- *   channel_idx    : int32 [num_kv_heads][r] = C, ascending, distinct.   */
+ *                    (DS_LABEL_INT4: packed codes, see ds_label_format)
+ *   channel_idx    : int32 [num_kv_heads][r] = C, ascending, distinct.
+ *   label_format   : ds_label_format (0 = native: a zero-initialised
+ *                    struct keeps the 16-bit label)
+ *   label_scale    : DS_LABEL_INT4 only: dtype [batch][num_kv_heads][max_seq_len],
+ *                    16-B aligned; ignored (may be NULL) for native labels. */
 typedef struct {
   int32_t batch, num_q_heads, num_kv_heads, head_dim;
   int32_t page_size, num_pages, max_pages_per_seq, max_seq_len, r;
@@ -77,6 +101,8 @@ typedef struct {
   const int32_t *seq_lens;
   void *label;
   const int32_t *channel_idx;
+  ds_label_format label_format;
+  void *label_scale;
 } ds_cache;
 
 /* Human-readable name of a status code (static string, never NULL). */
@@ -105,7 +131,9 @@ ds_status ds_calibrate_channels(const void *q_calib, const void *k_calib, int32_
  * in the decoding phase, only the heavy channel values of new tokens are
  * added."  For every b < batch, i < n_new, h: token p = positions[b] + i
  * gets K/V rows k_new[b][i][h][:], v_new[b][i][h][:] written into its
- * page slot and label[b][h][p][j] = k_new[b][i][h][C[h][j]] (a bit copy).
+ * page slot and label[b][h][p][j] = k_new[b][i][h][C[h][j]] (a bit copy;
+ * DS_LABEL_INT4: the row's codes and scale quantised from those values,
+ * reading R16).
  *   k_new, v_new : [batch][n_new][num_kv_heads][head_dim]
  *   positions    : int32 [batch] (device), first write position per
  *                  sequence; p < max_seq_len and its page must be mapped.

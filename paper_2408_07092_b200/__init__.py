@@ -22,6 +22,8 @@ DS_OK, DS_ERR_INVALID_ARGUMENT, DS_ERR_UNSUPPORTED, DS_ERR_GQA_INCOMPATIBLE, \
     DS_ERR_WORKSPACE_TOO_SMALL, DS_ERR_CUDA = range(6)
 DS_FP16, DS_BF16, DS_FP32 = 0, 1, 2
 DS_CALIB_QK, DS_CALIB_Q, DS_CALIB_K, DS_CALIB_RANDOM = 0, 1, 2, 3
+DS_LABEL_NATIVE, DS_LABEL_INT4 = 0, 1
+_LF = {"native": DS_LABEL_NATIVE, "int4": DS_LABEL_INT4}
 
 _DT = {torch.float16: DS_FP16, torch.bfloat16: DS_BF16, torch.float32: DS_FP32}
 
@@ -44,7 +46,8 @@ class ds_cache(ctypes.Structure):
                 ("r", ctypes.c_int32), ("dtype", ctypes.c_int),
                 ("k_pool", ctypes.c_void_p), ("v_pool", ctypes.c_void_p),
                 ("block_table", ctypes.c_void_p), ("seq_lens", ctypes.c_void_p),
-                ("label", ctypes.c_void_p), ("channel_idx", ctypes.c_void_p)]
+                ("label", ctypes.c_void_p), ("channel_idx", ctypes.c_void_p),
+                ("label_format", ctypes.c_int), ("label_scale", ctypes.c_void_p)]
 
 
 _lib = None
@@ -140,12 +143,18 @@ class LayerCache:
     seq_lens: torch.Tensor
     label: torch.Tensor
     channel_idx: torch.Tensor
+    label_format: int = DS_LABEL_NATIVE
+    label_scale: torch.Tensor | None = None
 
     @staticmethod
     def allocate(batch, num_q_heads, num_kv_heads, head_dim, max_seq_len, r, dtype, block_table,
-                 num_pages=None, page_size=16, device="cuda", channel_idx=None, host_kv=False):
+                 num_pages=None, page_size=16, device="cuda", channel_idx=None, host_kv=False,
+                 label_format="native"):
         """host_kv: K/V pools in pinned host memory (Double Sparsity-Offload,
-        P:192): the kernels read them over the host link; label stays on device."""
+        P:192): the kernels read them over the host link; label stays on device.
+        label_format: "native" (label in K's dtype) or "int4" (packed 4-bit
+        codes uint8 [B][Hkv][S][ceil(r/2)] + a per-token scale [B][Hkv][S],
+        P:171, ds.h ds_label_format)."""
         bt = torch.as_tensor(block_table, dtype=torch.int32).to(device).contiguous()
         npages = int(num_pages if num_pages is not None else int(bt.max()) + 1)
         pool = (npages, num_kv_heads, page_size, head_dim)
@@ -154,13 +163,20 @@ class LayerCache:
             if host_kv:
                 return torch.empty(pool, dtype=dtype, pin_memory=True)
             return torch.empty(pool, dtype=dtype, device=device)
+        lf = _LF[label_format] if isinstance(label_format, str) else int(label_format)
+        if lf == DS_LABEL_INT4:
+            label = torch.empty((batch, num_kv_heads, max_seq_len, (r + 1) // 2), dtype=torch.uint8, device=device)
+            scale = torch.empty((batch, num_kv_heads, max_seq_len), dtype=dtype, device=device)
+        else:
+            label = torch.empty((batch, num_kv_heads, max_seq_len, r), dtype=dtype, device=device)
+            scale = None
         return LayerCache(
             batch, num_q_heads, num_kv_heads, head_dim, page_size, max_seq_len, r, dtype,
             pool_buf(), pool_buf(),
-            bt, torch.zeros(batch, dtype=torch.int32, device=device),
-            torch.empty((batch, num_kv_heads, max_seq_len, r), dtype=dtype, device=device),
+            bt, torch.zeros(batch, dtype=torch.int32, device=device), label,
             (torch.as_tensor(channel_idx, dtype=torch.int32).to(device).contiguous() if channel_idx is not None
-             else torch.zeros((num_kv_heads, r), dtype=torch.int32, device=device)))
+             else torch.zeros((num_kv_heads, r), dtype=torch.int32, device=device)),
+            lf, scale)
 
     @property
     def num_pages(self):
@@ -170,7 +186,13 @@ class LayerCache:
         return ds_cache(self.batch, self.num_q_heads, self.num_kv_heads, self.head_dim, self.page_size,
                         self.num_pages, self.block_table.shape[1], self.max_seq_len, self.r,
                         _DT[self.dtype], _ptr(self.k_pool), _ptr(self.v_pool), _ptr(self.block_table),
-                        _ptr(self.seq_lens), _ptr(self.label), _ptr(self.channel_idx))
+                        _ptr(self.seq_lens), _ptr(self.label), _ptr(self.channel_idx), self.label_format,
+                        _ptr(self.label_scale))
+
+    @property
+    def label_bytes(self) -> int:
+        n = self.label.numel() * self.label.element_size()
+        return n + (self.label_scale.numel() * self.label_scale.element_size() if self.label_scale is not None else 0)
 
 
 def ds_calibrate_channels(q_calib, k_calib, num_kv_heads, r, mode=DS_CALIB_QK, seed=0, out=None, stream=None):

@@ -67,9 +67,11 @@ def build_trace() -> str:
     with open(unity, "w") as f:
         for src in _sources():
             f.write('#include "%s"\n' % src)
-    out = os.path.join(PKG, "libds_trace.so")
-    subprocess.check_call([NVCC, *ARCH, *[x for x in FLAGS if x not in ("-v", "-Xptxas")], "-DDS_TRACE", "-shared", unity,
-                           "-o", out])
+    # DS_TRACE_FLAGS / DS_TRACE_NAME: extra -D switches of timing experiments
+    out = os.path.join(PKG, os.environ.get("DS_TRACE_NAME", "libds_trace.so"))
+    extra = os.environ.get("DS_TRACE_FLAGS", "").split()
+    subprocess.check_call([NVCC, *ARCH, *[x for x in FLAGS if x not in ("-v", "-Xptxas")], "-DDS_TRACE", *extra,
+                           "-shared", unity, "-o", out])
     return out
 
 

@@ -28,6 +28,9 @@ CacheView make_view(const ds_cache *c) {
   v.seq_lens = c->seq_lens;
   v.label = c->label;
   v.C = c->channel_idx;
+  v.lq4 = c->label_format == DS_LABEL_INT4;
+  v.rb = (c->r + 1) / 2;
+  v.label_scale = c->label_scale;
   return v;
 }
 
@@ -72,6 +75,9 @@ static ds_status validate_cache(const ds_cache *c) {
   if (!c->k_pool || !c->v_pool || !c->block_table || !c->seq_lens || !c->label || !c->channel_idx)
     return DS_ERR_INVALID_ARGUMENT;
   if (!aligned16(c->k_pool) || !aligned16(c->v_pool) || !aligned16(c->label)) return DS_ERR_INVALID_ARGUMENT;
+  if (c->label_format != DS_LABEL_NATIVE && c->label_format != DS_LABEL_INT4) return DS_ERR_INVALID_ARGUMENT;
+  if (c->label_format == DS_LABEL_INT4 && (!c->label_scale || !aligned16(c->label_scale)))
+    return DS_ERR_INVALID_ARGUMENT;
   return DS_OK;
 }
 

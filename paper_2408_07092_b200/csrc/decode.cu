@@ -44,6 +44,12 @@ namespace cg = cooperative_groups;
 namespace ds {
 namespace fused {
 
+#ifdef DS_EXP_NOHIST  // timing experiment only (wrong results): no digit-1 histogram
+#define DS_HIST_ADD(p) ((void)(p))
+#else
+#define DS_HIST_ADD(p) atomicAdd((p), 1u)
+#endif
+
 constexpr int kThreads = 1024;
 constexpr int kWarps = kThreads / 32;
 constexpr int kAttWarps = 16;  // warps [0, 16): attention; [16, 32): selection tail
@@ -166,9 +172,44 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   pdl_wait();  // label / KV rows may come from the preceding append
   // (dependents are released only after the register split below: a CTA of
   // the next kernel must not take the registers the selection warps free)
+  const int t0 = crank * p.chunk;  // this CTA's tokens [t0, t0 + nloc)
+  const size_t lrow = ((size_t)b * c.Hkv + h) * (size_t)c.Smax + t0;  // first label row of this CTA
+  const T *lab = (const T *)c.label + lrow * (size_t)c.r;
+  const uint8_t *cod = (const uint8_t *)c.label + lrow * (size_t)c.rb;  // 4-bit label (R16)
+  const T *scl = (const T *)c.label_scale + lrow;
+  // The first label batch is requested before anything else waits on memory,
+  // so the prologue's round trips (seq_lens, C, q) overlap it.  Its bound is
+  // the allocation (Smax), not seq_lens: rows past the sequence are read and
+  // dropped below.
+  const int maxloc = max(0, min(p.chunk, c.Smax - t0));
+  constexpr bool kVec16 = R > 0 && R * sizeof(T) == 16;  // one 16-B label row per token
+  constexpr int U = kUnroll;
+  const bool q4v = R == 8 && c.lq4 && (c.Smax & 3) == 0;  // 16-B code / 8-B scale vectors of 4 tokens
+  // one register array for both label formats (int4: codes of two groups in
+  // pv[0..1], their scales in pv[2])
+  uint4 pv[U];
+  bool pre = false;
+  if (!c.lq4) {
+    if constexpr (kVec16) {
+      pre = tid + (U - 1) * kThreads < maxloc;
+      if (pre) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) pv[u] = ldg_nc_v4(reinterpret_cast<const uint4 *>(lab) + tid + u * kThreads);
+      }
+    }
+  } else if (q4v) {
+    const int mg = maxloc >> 2;
+    const uint2 z2 = make_uint2(0, 0);
+    uint2 a2 = z2, b2 = z2;
+    pv[0] = pv[1] = make_uint4(0, 0, 0, 0);
+    if (tid < mg) pv[0] = ldg_nc_v4(reinterpret_cast<const uint4 *>(cod) + tid), a2 = ldg_nc_v2(reinterpret_cast<const uint2 *>(scl) + tid);
+    if (tid + kThreads < mg)
+      pv[1] = ldg_nc_v4(reinterpret_cast<const uint4 *>(cod) + tid + kThreads),
+      b2 = ldg_nc_v2(reinterpret_cast<const uint2 *>(scl) + tid + kThreads);
+    pv[2] = make_uint4(a2.x, a2.y, b2.x, b2.y);
+  }
   const int n = c.seq_lens[b];
   const int keff = min(p.k, n);
-  const int t0 = crank * p.chunk;                // this CTA's tokens [t0, t0 + nloc)
   const int nloc = max(0, min(p.chunk, n - t0));
   T *outp = (T *)p.out + ((size_t)b * c.Hq + (size_t)h * G) * D;
   int32_t *idx = p.idx ? p.idx + (size_t)unit * p.k : nullptr;
@@ -182,15 +223,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     return;
   }
 
-  // ---- a1, query tile, zeroing
+  // ---- a1, query tile, zeroing (the tile and C are loaded together; q_lab
+  // is then summed from the tile in shared memory)
   const T *qb = (const T *)p.q + ((size_t)b * c.Hq + (size_t)h * G) * D;
   const int r = R > 0 ? R : c.r;
-  for (int j = tid; j < r; j += kThreads) {
-    const int ch = c.C[(size_t)h * c.r + j];
-    float s = 0.0f;
-    for (int g = 0; g < G; ++g) s = s + Elem<T>::to_f(qb[(size_t)g * D + ch]);
-    sh.qlab[j] = s;
-  }
+  int chj = 0;
+  if (tid < r) chj = c.C[(size_t)h * c.r + tid];
   for (int i = tid; i < 8 * CHN; i += kThreads) {
     const int row = i / CHN, ch = i - (i / CHN) * CHN;
     const uint4 v = row < G ? reinterpret_cast<const uint4 *>(qb + (size_t)row * D)[ch] : make_uint4(0, 0, 0, 0);
@@ -206,6 +244,14 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     sh.lower_sel = 0;
   }
   __syncthreads();
+  for (int j = tid; j < r; j += kThreads) {  // Q_label[j] = sum_g q[g][C[j]], g ascending (R3)
+    const int ch = j == tid ? chj : c.C[(size_t)h * c.r + j];
+    float s = 0.0f;
+    for (int g = 0; g < G; ++g)
+      s = s + Elem<T>::to_f(*reinterpret_cast<const T *>(sh.qt + g * ROWB + swz(g, ch >> 3) + (ch & 7) * 2));
+    sh.qlab[j] = s;
+  }
+  __syncthreads();
   float ql[R > 0 ? R : 1];
   if constexpr (R > 0) {
 #pragma unroll
@@ -213,16 +259,51 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   }
   const float *qs = R > 0 ? ql : sh.qlab;
 
+  DS_TRACE_AT(1, 12);
   // ---- a2: stream this CTA's label rows -> order keys + digit-1 histogram
-  const T *lab = (const T *)c.label + (((size_t)b * c.Hkv + h) * (size_t)c.Smax + t0) * (size_t)c.r;
-  {
+  if (c.lq4) {
+    // 4-bit label (reading R16): ceil(r/2) code bytes + one scale per
+    // token; s_hat = (fma chain of q_label[j] * c_j) * s
     int i0 = tid;
-    if constexpr (R > 0 && R * sizeof(T) == 16) {
-      constexpr int U = kUnroll;
-      for (; i0 + (U - 1) * kThreads < nloc; i0 += U * kThreads) {
-        uint4 v[U];
+    if (q4v) {
+      const uint4 *cv = reinterpret_cast<const uint4 *>(cod);
+      const uint2 *sv = reinterpret_cast<const uint2 *>(scl);
+      const int ng = nloc >> 2;
+      auto grp = [&](int g, const uint4 &v, const uint2 &w) {
+        const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+        const T *se = reinterpret_cast<const T *>(&w);
+        uint32_t kk[4];
 #pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = __ldg(reinterpret_cast<const uint4 *>(lab) + (size_t)(i0 + u * kThreads));
+        for (int e = 0; e < 4; ++e) {
+          kk[e] = order_key(q4_word_dot(wd[e], ql, 0.0f) * Elem<T>::to_f(se[e]));
+          DS_HIST_ADD(&sh.h1[kk[e] >> kSh1]);
+        }
+        *reinterpret_cast<uint4 *>(keys + 4 * g) = make_uint4(kk[0], kk[1], kk[2], kk[3]);
+      };
+      // two groups per thread in flight while the previous two are scored
+      uint4 v0 = pv[0], v1 = pv[1];
+      uint2 w0 = make_uint2(pv[2].x, pv[2].y), w1 = make_uint2(pv[2].z, pv[2].w);
+      int g0 = tid;
+      for (; g0 < ng; g0 += 2 * kThreads) {
+        uint4 n0 = v0, n1 = v1;
+        uint2 m0 = w0, m1 = w1;
+        if (g0 + 2 * kThreads < ng) n0 = ldg_nc_v4(cv + g0 + 2 * kThreads), m0 = ldg_nc_v2(sv + g0 + 2 * kThreads);
+        if (g0 + 3 * kThreads < ng) n1 = ldg_nc_v4(cv + g0 + 3 * kThreads), m1 = ldg_nc_v2(sv + g0 + 3 * kThreads);
+        grp(g0, v0, w0);
+        if (g0 + kThreads < ng) grp(g0 + kThreads, v1, w1);
+        v0 = n0, v1 = n1, w0 = m0, w1 = m1;
+      }
+      i0 = 4 * ng + tid;
+    }
+    for (int i = i0; i < nloc; i += kThreads) {
+      const uint32_t k0 = order_key(q4_score<T>(cod + (size_t)i * c.rb, scl[i], qs, r));
+      keys[i] = k0;
+      DS_HIST_ADD(&sh.h1[k0 >> kSh1]);
+    }
+  } else {
+    int i0 = tid;
+    if constexpr (kVec16) {
+      auto rows8 = [&](int ib, const uint4 (&v)[U]) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const T *e = reinterpret_cast<const T *>(&v[u]);
@@ -230,9 +311,18 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
 #pragma unroll
           for (int j = 0; j < R; ++j) s = fmaf(ql[j], Elem<T>::to_f(e[j]), s);
           const uint32_t k0 = order_key(s);
-          keys[i0 + u * kThreads] = k0;
-          atomicAdd(&sh.h1[k0 >> kSh1], 1u);
+          keys[ib + u * kThreads] = k0;
+          DS_HIST_ADD(&sh.h1[k0 >> kSh1]);
         }
+      };
+      if (pre && i0 + (U - 1) * kThreads < nloc) {  // the prefetched first batch
+        rows8(i0, pv);
+        i0 += U * kThreads;
+      }
+      for (; i0 + (U - 1) * kThreads < nloc; i0 += U * kThreads) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) pv[u] = __ldg(reinterpret_cast<const uint4 *>(lab) + (size_t)(i0 + u * kThreads));
+        rows8(i0, pv);
       }
     }
     for (int i = i0; i < nloc; i += kThreads) {
@@ -241,9 +331,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       for (int j = 0; j < r; ++j) s = fmaf(qs[j], Elem<T>::to_f(row[j]), s);
       const uint32_t k0 = order_key(s);
       keys[i] = k0;
-      atomicAdd(&sh.h1[k0 >> kSh1], 1u);
+      DS_HIST_ADD(&sh.h1[k0 >> kSh1]);
     }
   }
+  DS_TRACE_AT(1, 13);
   if (tid < 128) keys[nloc + tid] = 0u;  // pad: below every finite score's key
   __syncthreads();
   DS_TRACE_AT(1, 1);

@@ -170,6 +170,66 @@ __device__ __forceinline__ uint32_t order_key(float s) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+// ---------------------------------------------- 4-bit label (reading R16)
+// code j of a packed row: nibble j (byte j/2, low nibble first), 4-bit
+// two's complement
+__device__ __forceinline__ int q4_code(const uint8_t *row, int j) {
+  const int by = row[j >> 1];
+  return (j & 1) ? ((int)(int8_t)by >> 4) : ((int)(int8_t)(by << 4) >> 4);
+}
+// fma chain over the 8 codes of a packed word (j ascending), each code
+// exact and without an int->float conversion (I2F is a low-throughput pipe).
+// a = w ^ 0x88888888 holds u_j = c_j + 8 in [1, 15] in nibble j.  Nibble j at
+// bits [4j, 4j + 4) (j <= 4), masked out and OR-ed with the exponent of
+// 2^(23 - 4j), is the float 2^(23 - 4j) + u_j exactly (its lowest set
+// mantissa bit weighs 1), so c_j = that - (2^(23 - 4j) + 8); nibbles 5..7 do
+// the same on a >> 20.  One LOP3 + one FADD per code, one SHF per word.
+template <uint32_t MASK>
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t orv) {
+  uint32_t d;  // (a & MASK) | orv in one LOP3
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "n"(MASK), "r"(orv));
+  return d;
+}
+__device__ __forceinline__ float q4_word_dot(uint32_t w, const float *ql, float acc) {
+  const uint32_t a = w ^ 0x88888888u, b = a >> 20;
+  const float c0 = __uint_as_float(lop3_and_or<0x0000Fu>(a, 0x4B000000u)) - 8388616.0f;  // 2^23 + 8
+  const float c1 = __uint_as_float(lop3_and_or<0x000F0u>(a, 0x49000000u)) - 524296.0f;   // 2^19 + 8
+  const float c2 = __uint_as_float(lop3_and_or<0x00F00u>(a, 0x47000000u)) - 32776.0f;    // 2^15 + 8
+  const float c3 = __uint_as_float(lop3_and_or<0x0F000u>(a, 0x45000000u)) - 2056.0f;     // 2^11 + 8
+  const float c4 = __uint_as_float(lop3_and_or<0xF0000u>(a, 0x43000000u)) - 136.0f;      // 2^7 + 8
+  const float c5 = __uint_as_float(lop3_and_or<0x0000Fu>(b, 0x4B000000u)) - 8388616.0f;
+  const float c6 = __uint_as_float(lop3_and_or<0x000F0u>(b, 0x49000000u)) - 524296.0f;
+  const float c7 = __uint_as_float(lop3_and_or<0x00F00u>(b, 0x47000000u)) - 32776.0f;
+  acc = fmaf(ql[0], c0, acc);
+  acc = fmaf(ql[1], c1, acc);
+  acc = fmaf(ql[2], c2, acc);
+  acc = fmaf(ql[3], c3, acc);
+  acc = fmaf(ql[4], c4, acc);
+  acc = fmaf(ql[5], c5, acc);
+  acc = fmaf(ql[6], c6, acc);
+  acc = fmaf(ql[7], c7, acc);
+  return acc;
+}
+// 16-B / 8-B read-only loads issued where they are written (asm volatile:
+// the compiler cannot sink a prefetch below the work it overlaps)
+__device__ __forceinline__ uint4 ldg_nc_v4(const void *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];\n" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ldg_nc_v2(const void *p) {
+  uint2 r;
+  asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];\n" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+// line 2 over a 4-bit label row: (fp32 fma chain of q_label[j] * c_j) * s
+template <typename T>
+__device__ __forceinline__ float q4_score(const uint8_t *row, T scale, const float *ql, int r) {
+  float acc = 0.0f;
+  for (int j = 0; j < r; ++j) acc = fmaf(ql[j], (float)q4_code(row, j), acc);
+  return acc * Elem<T>::to_f(scale);
+}
+
 // Inverse of order_key (the canonical +0 for the zero key).
 __device__ __forceinline__ float key_to_float(uint32_t key) {
   const uint32_t u = (key & 0x80000000u) ? (key & 0x7fffffffu) : ~key;

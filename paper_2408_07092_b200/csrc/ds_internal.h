@@ -14,6 +14,8 @@ struct CacheView {
   const int32_t *block_table, *seq_lens;
   const void *label;
   const int32_t *C;
+  int lq4, rb;              // DS_LABEL_INT4; code bytes per label row (ceil(r/2))
+  const void *label_scale;  // DS_LABEL_INT4: [B][Hkv][Smax] of the cache dtype
 };
 
 // score_select_kernel: a1 + a2 + a3 -> index list + pool row ids per unit.

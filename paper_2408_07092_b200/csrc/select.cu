@@ -185,17 +185,23 @@ __global__ void __launch_bounds__(kThreads, 2) score_select_kernel(ScoreParams p
     for (int j = 0; j < R; ++j) ql[j] = sh.qlab[j];
   }
   const float *qs = R > 0 ? ql : sh.qlab;
-  const T *lab = (const T *)c.label + (((size_t)b * c.Hkv + h) * c.Smax + t0) * (size_t)c.r;
+  const size_t lrow = ((size_t)b * c.Hkv + h) * c.Smax + t0;  // first label row of this CTA
+  const T *lab = (const T *)c.label + lrow * (size_t)c.r;
+  const uint8_t *cod = (const uint8_t *)c.label + lrow * (size_t)c.rb;  // 4-bit label (R16)
+  const T *scl = (const T *)c.label_scale + lrow;
+  auto score_at = [&](int i) {
+    return c.lq4 ? q4_score<T>(cod + (size_t)i * c.rb, scl[i], qs, r) : label_score<T, R>(lab + (size_t)i * r, qs, r);
+  };
   if (p.scores) {  // diagnostics entry (ds_approx_scores): s_hat to HBM
     float *so = p.scores + (size_t)unit * c.Smax + t0;
-    for (int i = tid; i < nloc; i += kThreads) so[i] = label_score<T, R>(lab + (size_t)i * r, qs, r);
+    for (int i = tid; i < nloc; i += kThreads) so[i] = score_at(i);
     return;
   }
   // ---- a2: stream the label -> keys + level-1 histogram
   int i0 = tid;
   if constexpr (R > 0 && R * sizeof(T) == 16) {
     constexpr int U = kUnroll;
-    for (; i0 + (U - 1) * kThreads < nloc; i0 += U * kThreads) {
+    for (; !c.lq4 && i0 + (U - 1) * kThreads < nloc; i0 += U * kThreads) {
       uint4 v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = __ldg(reinterpret_cast<const uint4 *>(lab) + (size_t)(i0 + u * kThreads));
@@ -212,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 2) score_select_kernel(ScoreParams p
     }
   }
   for (int i = i0; i < nloc; i += kThreads) {
-    const uint32_t k0 = order_key(label_score<T, R>(lab + (size_t)i * r, qs, r));
+    const uint32_t k0 = order_key(score_at(i));
     keys[i] = k0;
     atomicAdd(&sh.h1[k0 >> kSh1], 1u);
   }

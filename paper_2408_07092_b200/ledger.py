@@ -9,33 +9,38 @@ size e (the label has K's dtype, DESIGN reading R8):
     B_dense = 2*S*d*e                             (+ q/out, same as above)
 
 Top-k moves no algorithmic bytes.  k is per sequence:
-k_eff = min(k, S_b).
+k_eff = min(k, S_b).  With the 4-bit label (reading R16) a label row
+is ceil(r/2) code bytes + one e-byte scale: S*r*e becomes S*(ceil(r/2) + e).
 """
 from __future__ import annotations
 
 
-def unit_bytes_alg(S: int, d: int, r: int, k: int, e: int) -> int:
-    keff = min(k, S)
-    return S * r * e + 2 * keff * d * e
+def label_row_bytes(r: int, e: int, label: str = "native") -> int:
+    return (r + 1) // 2 + e if label == "int4" else r * e
 
 
-def unit_bytes_all(S: int, d: int, r: int, k: int, e: int, G: int) -> int:
+def unit_bytes_alg(S: int, d: int, r: int, k: int, e: int, label: str = "native") -> int:
     keff = min(k, S)
-    return unit_bytes_alg(S, d, r, k, e) + 2 * G * d * e + 4 * keff
+    return S * label_row_bytes(r, e, label) + 2 * keff * d * e
+
+
+def unit_bytes_all(S: int, d: int, r: int, k: int, e: int, G: int, label: str = "native") -> int:
+    keff = min(k, S)
+    return unit_bytes_alg(S, d, r, k, e, label) + 2 * G * d * e + 4 * keff
 
 
 def unit_bytes_dense(S: int, d: int, e: int) -> int:
     return 2 * S * d * e
 
 
-def layer_bytes_alg(cfg) -> int:
-    return cfg.B * cfg.Hkv * unit_bytes_alg(cfg.S, cfg.d, cfg.r, cfg.k, cfg.elem)
+def layer_bytes_alg(cfg, label: str = "native") -> int:
+    return cfg.B * cfg.Hkv * unit_bytes_alg(cfg.S, cfg.d, cfg.r, cfg.k, cfg.elem, label)
 
 
 def layer_bytes_dense(cfg) -> int:
     return cfg.B * cfg.Hkv * unit_bytes_dense(cfg.S, cfg.d, cfg.elem)
 
 
-def byte_ratio_ceiling(cfg) -> float:
+def byte_ratio_ceiling(cfg, label: str = "native") -> float:
     """Upper bound of the sparse/dense speedup at equal achieved bandwidth."""
-    return layer_bytes_dense(cfg) / layer_bytes_alg(cfg)
+    return layer_bytes_dense(cfg) / layer_bytes_alg(cfg, label)

@@ -21,7 +21,8 @@ for kv in sys.argv[2:]:  # overrides, e.g. B=1 Hkv=1 Hq=4
 print(cfg)
 lay = synth.make_layer(cfg, cfg.seed_base, device="cuda")
 cache = ds.LayerCache.allocate(cfg.B, cfg.Hq, cfg.Hkv, cfg.d, cfg.S, cfg.r, synth.DTYPES[cfg.dtype], lay.block_table,
-                               num_pages=lay.num_pages, page_size=cfg.page_size, channel_idx=lay.C_plant)
+                               num_pages=lay.num_pages, page_size=cfg.page_size, channel_idx=lay.C_plant,
+                               label_format=os.environ.get("DS_LABEL", "native"))
 ds.prefill(cache, lay.K, lay.V, lay.seq_lens)
 del lay.K, lay.V
 L = ds.lib()
@@ -95,5 +96,5 @@ def report1():
             prev = s_
 report(2, ["start", "rowids", "loop done", "cluster sync", "merged"])
 report(1, ["start", "streamed", "masks", "tail done", "gt rows done", "all rows", "merged"])
-report_slots(1, [(1, 7, "D1 boundary"), (7, 8, "mask loop w0"), (8, 9, "cand gather w0"), (9, 2, "sync"),
+report_slots(1, [(0, 12, "prologue"), (12, 13, "stream t0"), (13, 1, "stream sync"), (1, 7, "D1 boundary"), (7, 8, "mask loop w0"), (8, 9, "cand gather w0"), (9, 2, "sync"),
                  (2, 3, "tail"), (5, 10, "partials"), (10, 11, "weights"), (11, 6, "outputs")])

@@ -15,13 +15,13 @@ TOL = {"fp32": (1e-5, 1e-4), "fp16": (2e-3, 1e-2), "bf16": (2e-3, 1e-2)}   # (at
 
 
 def build_cache(cfg: synth.Config, seed=None, structure="iid", seq_lens=None, C=None, identity_pages=False,
-                device="cuda"):
+                device="cuda", label_format="native"):
     lay = synth.make_layer(cfg, seed, device=device, structure=structure, seq_lens=seq_lens,
                            identity_pages=identity_pages)
     C = lay.C_plant if C is None else torch.as_tensor(C, dtype=torch.int32)
     cache = ds.LayerCache.allocate(cfg.B, cfg.Hq, cfg.Hkv, cfg.d, cfg.S, cfg.r, synth.DTYPES[cfg.dtype],
                                    lay.block_table, num_pages=lay.num_pages, page_size=cfg.page_size,
-                                   device=device, channel_idx=C)
+                                   device=device, channel_idx=C, label_format=label_format)
     ds.prefill(cache, lay.K, lay.V, lay.seq_lens)
     return lay, cache, C
 
@@ -76,7 +76,10 @@ def check_units(lay, cache, C, k, units, y_gpu, idx_gpu):
             assert np.all(idx_gpu[b, h] == -1) and np.all(y_gpu[b, h * G:(h + 1) * G] == 0)
             continue
         L = oracle.label_gather(K, Ch[h])
-        y_ref, idx_ref, shat, tau = oracle.ds_decode_unit(q, K, V, L, Ch[h], k)
+        codes = scale = None
+        if cache.label_format == ds.DS_LABEL_INT4:  # line 2 over the 4-bit label (R16)
+            codes, scale = oracle.quantize_label_4bit(L, cfg.dtype)
+        y_ref, idx_ref, shat, tau = oracle.ds_decode_unit(q, K, V, L, Ch[h], k, codes=codes, scale=scale)
         keff = min(k, S)
         nsym += check_selection(idx_gpu[b, h], idx_ref, shat, tau, keff)
         # attention checked on the GPU's own index set (truncated oracle)

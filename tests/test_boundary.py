@@ -65,6 +65,9 @@ def _cache(**kw):
     (dict(max_pages_per_seq=2), ds.DS_ERR_INVALID_ARGUMENT),            # 32 < 64 tokens
     (dict(label=0x5008), ds.DS_ERR_INVALID_ARGUMENT),                    # misaligned
     (dict(dtype=7), ds.DS_ERR_UNSUPPORTED),
+    (dict(label_format=2), ds.DS_ERR_INVALID_ARGUMENT),                  # unknown label format
+    (dict(label_format=ds.DS_LABEL_INT4), ds.DS_ERR_INVALID_ARGUMENT),   # int4 without a scale array
+    (dict(label_format=ds.DS_LABEL_INT4, label_scale=0xa008), ds.DS_ERR_INVALID_ARGUMENT),  # misaligned scale
 ])
 def test_decode_validation(kw, status):
     c = _cache(**kw)
@@ -98,3 +101,17 @@ def test_python_binding_refuses_cpu_tensors():
     import torch
     with pytest.raises(ValueError):
         ds._ptr(torch.zeros(4))
+
+
+def test_ds_cache_struct_layout_matches_header():
+    """The ctypes mirror of ds_cache has the header's field order; the two
+    label fields added for the 4-bit label (ds_label_format) come last, so
+    a zero-initialised struct keeps the native label."""
+    names = [f[0] for f in ds.ds_cache._fields_]
+    hdr = open(os.path.join(os.path.dirname(ds.LIB_PATH), "..", "include", "ds.h")).read()
+    body = hdr[hdr.index("typedef struct {\n  int32_t batch"):]
+    body = body[:body.index("} ds_cache;")]
+    decl = re.findall(r"\*?\s*(\w+)\s*[,;]", body)   # declarators in order
+    assert decl == names
+    assert names[-2:] == ["label_format", "label_scale"]
+    assert ds.ds_cache().label_format == ds.DS_LABEL_NATIVE
