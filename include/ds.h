@@ -71,8 +71,14 @@ typedef enum { DS_FP16 = 0, DS_BF16 = 1, DS_FP32 = 2 } ds_dtype;
  *                    label_scale : dtype [batch][num_kv_heads][max_seq_len] = s.
  *                    Line 2 becomes s_hat[t] = (fp32 fma chain over j of
  *                    q_label[j] * c_j) * s_t.  Per token ceil(r/2) + e bytes
- *                    instead of r * e (6 instead of 16 at r = 8, 16-bit). */
-typedef enum { DS_LABEL_NATIVE = 0, DS_LABEL_INT4 = 1 } ds_label_format;
+ *                    instead of r * e (6 instead of 16 at r = 8, 16-bit).
+ *   DS_LABEL_NONE  : no label cache (the ablation of Appendix B.1, Table 4,
+ *                    P:517-544): line 2 reads the r channels of each token
+ *                    straight from its paged K row (2-byte reads scattered
+ *                    over the row); label and label_scale are ignored and
+ *                    may be NULL.  Scores are the same values as with the
+ *                    native label (a bit copy of those channels). */
+typedef enum { DS_LABEL_NATIVE = 0, DS_LABEL_INT4 = 1, DS_LABEL_NONE = 2 } ds_label_format;
 
 /* Outlier-channel modes of Table 3: qk (default), q, k, random. */
 typedef enum { DS_CALIB_QK = 0, DS_CALIB_Q = 1, DS_CALIB_K = 2, DS_CALIB_RANDOM = 3 } ds_calib_mode;

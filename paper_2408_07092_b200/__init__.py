@@ -22,8 +22,8 @@ DS_OK, DS_ERR_INVALID_ARGUMENT, DS_ERR_UNSUPPORTED, DS_ERR_GQA_INCOMPATIBLE, \
     DS_ERR_WORKSPACE_TOO_SMALL, DS_ERR_CUDA = range(6)
 DS_FP16, DS_BF16, DS_FP32 = 0, 1, 2
 DS_CALIB_QK, DS_CALIB_Q, DS_CALIB_K, DS_CALIB_RANDOM = 0, 1, 2, 3
-DS_LABEL_NATIVE, DS_LABEL_INT4 = 0, 1
-_LF = {"native": DS_LABEL_NATIVE, "int4": DS_LABEL_INT4}
+DS_LABEL_NATIVE, DS_LABEL_INT4, DS_LABEL_NONE = 0, 1, 2
+_LF = {"native": DS_LABEL_NATIVE, "int4": DS_LABEL_INT4, "none": DS_LABEL_NONE}
 
 _DT = {torch.float16: DS_FP16, torch.bfloat16: DS_BF16, torch.float32: DS_FP32}
 
@@ -152,9 +152,10 @@ class LayerCache:
                  label_format="native"):
         """host_kv: K/V pools in pinned host memory (Double Sparsity-Offload,
         P:192): the kernels read them over the host link; label stays on device.
-        label_format: "native" (label in K's dtype) or "int4" (packed 4-bit
+        label_format: "native" (label in K's dtype), "int4" (packed 4-bit
         codes uint8 [B][Hkv][S][ceil(r/2)] + a per-token scale [B][Hkv][S],
-        P:171, ds.h ds_label_format)."""
+        P:171) or "none" (no label cache, the Table 4 ablation); ds.h
+        ds_label_format."""
         bt = torch.as_tensor(block_table, dtype=torch.int32).to(device).contiguous()
         npages = int(num_pages if num_pages is not None else int(bt.max()) + 1)
         pool = (npages, num_kv_heads, page_size, head_dim)
@@ -164,7 +165,10 @@ class LayerCache:
                 return torch.empty(pool, dtype=dtype, pin_memory=True)
             return torch.empty(pool, dtype=dtype, device=device)
         lf = _LF[label_format] if isinstance(label_format, str) else int(label_format)
-        if lf == DS_LABEL_INT4:
+        if lf == DS_LABEL_NONE:  # no label cache (Table 4 ablation): a 16-B placeholder, never read
+            label = torch.empty(16, dtype=torch.uint8, device=device)
+            scale = None
+        elif lf == DS_LABEL_INT4:
             label = torch.empty((batch, num_kv_heads, max_seq_len, (r + 1) // 2), dtype=torch.uint8, device=device)
             scale = torch.empty((batch, num_kv_heads, max_seq_len), dtype=dtype, device=device)
         else:

@@ -29,6 +29,7 @@ CacheView make_view(const ds_cache *c) {
   v.label = c->label;
   v.C = c->channel_idx;
   v.lq4 = c->label_format == DS_LABEL_INT4;
+  v.lnone = c->label_format == DS_LABEL_NONE;
   v.rb = (c->r + 1) / 2;
   v.label_scale = c->label_scale;
   return v;
@@ -72,10 +73,12 @@ static ds_status validate_cache(const ds_cache *c) {
   if (c->r > 256) return DS_ERR_UNSUPPORTED;
   // pool row ids are 32-bit inside the kernels
   if ((long long)c->num_pages * c->num_kv_heads * c->page_size >= (1ll << 31)) return DS_ERR_UNSUPPORTED;
-  if (!c->k_pool || !c->v_pool || !c->block_table || !c->seq_lens || !c->label || !c->channel_idx)
+  if (c->label_format != DS_LABEL_NATIVE && c->label_format != DS_LABEL_INT4 && c->label_format != DS_LABEL_NONE)
     return DS_ERR_INVALID_ARGUMENT;
-  if (!aligned16(c->k_pool) || !aligned16(c->v_pool) || !aligned16(c->label)) return DS_ERR_INVALID_ARGUMENT;
-  if (c->label_format != DS_LABEL_NATIVE && c->label_format != DS_LABEL_INT4) return DS_ERR_INVALID_ARGUMENT;
+  const bool lab = c->label_format != DS_LABEL_NONE;
+  if (!c->k_pool || !c->v_pool || !c->block_table || !c->seq_lens || (lab && !c->label) || !c->channel_idx)
+    return DS_ERR_INVALID_ARGUMENT;
+  if (!aligned16(c->k_pool) || !aligned16(c->v_pool) || (lab && !aligned16(c->label))) return DS_ERR_INVALID_ARGUMENT;
   if (c->label_format == DS_LABEL_INT4 && (!c->label_scale || !aligned16(c->label_scale)))
     return DS_ERR_INVALID_ARGUMENT;
   return DS_OK;

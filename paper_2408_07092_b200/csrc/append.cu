@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(128) append_kernel(CacheView c, const T *__res
     kd[v] = ks[v];
     vd[v] = vs[v];
   }
+  if (c.lnone) return;  // no label cache (Table 4 ablation)
   const int32_t *C = c.C + (size_t)h * c.r;
   const size_t lrow = ((size_t)b * c.Hkv + h) * c.Smax + p;
   if (!c.lq4) {

@@ -189,7 +189,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   // pv[0..1], their scales in pv[2])
   uint4 pv[U];
   bool pre = false;
-  if (!c.lq4) {
+  if (c.lnone) {
+  } else if (!c.lq4) {
     if constexpr (kVec16) {
       pre = tid + (U - 1) * kThreads < maxloc;
       if (pre) {
@@ -243,6 +244,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     sh.nmem = 0;
     sh.lower_sel = 0;
   }
+  // DS_LABEL_NONE: the chunk's block-table entries (cand is free until the masks)
+  int32_t *btc = reinterpret_cast<int32_t *>(sh.cand);
+  const int pg0 = t0 / c.P;
+  const int npg = nloc > 0 ? (t0 + nloc - 1) / c.P - pg0 + 1 : 0;
+  const bool btc_ok = c.lnone && npg <= (int)(sizeof(sh.cand) / 4);
+  if (btc_ok)
+    for (int i = tid; i < npg; i += kThreads) btc[i] = __ldg(c.block_table + (size_t)b * c.maxp + pg0 + i);
   __syncthreads();
   for (int j = tid; j < r; j += kThreads) {  // Q_label[j] = sum_g q[g][C[j]], g ascending (R3)
     const int ch = j == tid ? chj : c.C[(size_t)h * c.r + j];
@@ -261,7 +269,51 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
 
   DS_TRACE_AT(1, 12);
   // ---- a2: stream this CTA's label rows -> order keys + digit-1 histogram
-  if (c.lq4) {
+  if (c.lnone) {
+    // no label cache (the Table 4 ablation): the r channels are
+    // read straight from each token's paged K row -- 2-byte reads scattered
+    // over the 256-B row, one DRAM sector or more per channel
+    const T *kp = (const T *)c.k_pool;
+    const int32_t *bt = c.block_table + (size_t)b * c.maxp;
+    auto krow = [&](int t) -> const T * {
+      const int pg = t / c.P;
+      const int32_t page = btc_ok ? btc[pg - pg0] : __ldg(bt + pg);
+      return kp + (((size_t)page * c.Hkv + h) * c.P + (t - pg * c.P)) * (size_t)D;
+    };
+    int i0 = tid;
+    if constexpr (R > 0) {
+      int chs[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) chs[j] = __ldg(c.C + (size_t)h * c.r + j);
+      constexpr int UN = 4;
+      for (; i0 + (UN - 1) * kThreads < nloc; i0 += UN * kThreads) {
+        T e[UN][R];
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          const T *kr = krow(t0 + i0 + u * kThreads);
+#pragma unroll
+          for (int j = 0; j < R; ++j) e[u][j] = __ldg(kr + chs[j]);
+        }
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          float s = 0.0f;
+#pragma unroll
+          for (int j = 0; j < R; ++j) s = fmaf(ql[j], Elem<T>::to_f(e[u][j]), s);
+          const uint32_t k0 = order_key(s);
+          keys[i0 + u * kThreads] = k0;
+          DS_HIST_ADD(&sh.h1[k0 >> kSh1]);
+        }
+      }
+    }
+    for (int i = i0; i < nloc; i += kThreads) {
+      const T *kr = krow(t0 + i);
+      float s = 0.0f;
+      for (int j = 0; j < r; ++j) s = fmaf(qs[j], Elem<T>::to_f(kr[c.C[(size_t)h * c.r + j]]), s);
+      const uint32_t k0 = order_key(s);
+      keys[i] = k0;
+      DS_HIST_ADD(&sh.h1[k0 >> kSh1]);
+    }
+  } else if (c.lq4) {
     // 4-bit label (reading R16): ceil(r/2) code bytes + one scale per
     // token; s_hat = (fma chain of q_label[j] * c_j) * s
     int i0 = tid;

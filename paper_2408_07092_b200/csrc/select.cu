@@ -190,6 +190,14 @@ __global__ void __launch_bounds__(kThreads, 2) score_select_kernel(ScoreParams p
   const uint8_t *cod = (const uint8_t *)c.label + lrow * (size_t)c.rb;  // 4-bit label (R16)
   const T *scl = (const T *)c.label_scale + lrow;
   auto score_at = [&](int i) {
+    if (c.lnone) {  // no label cache (Table 4 ablation): the channels of the paged K row
+      const int t = t0 + i;
+      const T *kr = (const T *)c.k_pool +
+                    (((size_t)__ldg(bt + t / c.P) * c.Hkv + h) * c.P + t % c.P) * (size_t)c.D;
+      float s = 0.0f;
+      for (int j = 0; j < r; ++j) s = fmaf(qs[j], Elem<T>::to_f(kr[c.C[(size_t)h * c.r + j]]), s);
+      return s;
+    }
     return c.lq4 ? q4_score<T>(cod + (size_t)i * c.rb, scl[i], qs, r) : label_score<T, R>(lab + (size_t)i * r, qs, r);
   };
   if (p.scores) {  // diagnostics entry (ds_approx_scores): s_hat to HBM
@@ -201,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 2) score_select_kernel(ScoreParams p
   int i0 = tid;
   if constexpr (R > 0 && R * sizeof(T) == 16) {
     constexpr int U = kUnroll;
-    for (; !c.lq4 && i0 + (U - 1) * kThreads < nloc; i0 += U * kThreads) {
+    for (; !c.lq4 && !c.lnone && i0 + (U - 1) * kThreads < nloc; i0 += U * kThreads) {
       uint4 v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = __ldg(reinterpret_cast<const uint4 *>(lab) + (size_t)(i0 + u * kThreads));

@@ -65,7 +65,8 @@ def _cache(**kw):
     (dict(max_pages_per_seq=2), ds.DS_ERR_INVALID_ARGUMENT),            # 32 < 64 tokens
     (dict(label=0x5008), ds.DS_ERR_INVALID_ARGUMENT),                    # misaligned
     (dict(dtype=7), ds.DS_ERR_UNSUPPORTED),
-    (dict(label_format=2), ds.DS_ERR_INVALID_ARGUMENT),                  # unknown label format
+    (dict(label_format=3), ds.DS_ERR_INVALID_ARGUMENT),                  # unknown label format
+    (dict(label=0), ds.DS_ERR_INVALID_ARGUMENT),                         # native label missing
     (dict(label_format=ds.DS_LABEL_INT4), ds.DS_ERR_INVALID_ARGUMENT),   # int4 without a scale array
     (dict(label_format=ds.DS_LABEL_INT4, label_scale=0xa008), ds.DS_ERR_INVALID_ARGUMENT),  # misaligned scale
 ])
