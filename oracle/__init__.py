@@ -55,6 +55,8 @@ def lib():
         L.oracle_approx_scores_q4.argtypes = [P, P, P, i, i, P]
         L.oracle_ds_decode_unit.argtypes = [P, P, i, P, P, P, P, P, P, i, i, i, i, P, P, P, P]
         L.oracle_ds_decode_unit.restype = i
+        L.oracle_ds_decode_unit_group.argtypes = [P, P, i, P, P, P, P, P, P, i, i, i, i, i, P, P, P]
+        L.oracle_ds_decode_unit_group.restype = i
         L.oracle_decode_batch.argtypes = [P, P, P, P, P, P, P, P, P, i, i, i, i, i, i, i, i, P, P, i]
         L.oracle_decode_batch.restype = i
         L.oracle_calibrate.argtypes = [P, P, i, i, i, i, i, i, ctypes.c_uint64, P, P]
@@ -180,6 +182,34 @@ def ds_decode_unit(q, K, V, L, C, k, q_sel=None, codes=None, scale=None):
     n = lib().oracle_ds_decode_unit(_p(q), _p(qs), G, _p(K), _p(V), _p(L), _p(codes), _p(scale), _p(C), S,
                                     d, L.shape[1], k, _p(y), _p(idx), _p(shat), _p(tau))
     return y, idx[:n], shat[:S], float(tau[0])
+
+
+GROUP_MODES = {"sum": 0, "max": 1, "per_head": 2}
+
+
+def ds_decode_unit_group(q, K, V, L, C, k, group="sum", q_sel=None, codes=None, scale=None):
+    """Algorithm 1 for one GQA unit under a group-reduction reading (R3 sum,
+    R17 max / per_head).  Returns (y [G][d], idx, shat): idx [k_eff] and
+    shat [S] for sum/max, idx [G][k] (-1 padded) and shat [G][S] per head."""
+    q = _f32(q)
+    if q.ndim == 1:
+        q = q[None]
+    qs = q if q_sel is None else _f32(q_sel).reshape(q.shape)
+    K, V, L, C = _f32(K), _f32(V), _f32(L), _i32(C)
+    if scale is not None:
+        codes = np.ascontiguousarray(codes, dtype=np.int8)
+        scale = _f32(scale)
+    S, d = K.shape
+    G = q.shape[0]
+    mode = GROUP_MODES[group]
+    y = np.empty((G, d), np.float32)
+    idx = np.empty((G, max(k, 1)) if mode == 2 else (max(1, min(k, S)),), np.int32)
+    shat = np.empty((G, max(S, 1)) if mode == 2 else (max(S, 1),), np.float32)
+    n = lib().oracle_ds_decode_unit_group(_p(q), _p(qs), G, _p(K), _p(V), _p(L), _p(codes), _p(scale), _p(C), S,
+                                          d, L.shape[1], k, mode, _p(y), _p(idx), _p(shat))
+    if mode == 2:
+        return y, idx[:, :k], shat[:, :S]
+    return y, idx[:n], shat[:S]
 
 
 def decode_batch(q, K, V, L, C, seq_lens, k, mode=0, q_sel=None, nthreads=1, codes=None, scale=None):

@@ -251,6 +251,61 @@ int oracle_ds_decode_unit(const float *q_attn, const float *q_sel, int G,
   return keff;
 }
 
+/* GQA selection granularity, reading R17 (the paper runs
+ * GQA models, Table 3, without saying how the G query heads of a
+ * KV head share the selection).  mode 0 = group sum (reading R3, exactly
+ * oracle_ds_decode_unit), 1 = max over the heads of the per-head scores,
+ * 2 = per head (each query head runs Algorithm 1 alone on the shared
+ * label/K/V).  Outputs: y [G][d]; idx_out [k_eff] (modes 0, 1) or
+ * [G][k] with -1 past each head's k_eff (mode 2); shat_out [S] (modes 0, 1)
+ * or [G][S] (mode 2).  Returns k_eff.                                    */
+int oracle_ds_decode_unit_group(const float *q_attn, const float *q_sel, int G,
+                                const float *K, const float *V, const float *L,
+                                const int8_t *codes, const float *scale,
+                                const int32_t *C, int S, int d, int r, int k,
+                                int mode, float *y, int32_t *idx_out,
+                                float *shat_out) {
+  if (mode == 0)
+    return oracle_ds_decode_unit(q_attn, q_sel, G, K, V, L, codes, scale, C, S, d, r, k, y,
+                                 idx_out, shat_out, NULL);
+  int keff = k < S ? k : S;
+  if (mode == 2) {
+    for (int g = 0; g < G; ++g) {
+      int32_t *ig = idx_out ? idx_out + (size_t)g * k : NULL;
+      oracle_ds_decode_unit(q_attn + (size_t)g * d, q_sel + (size_t)g * d, 1, K, V, L, codes,
+                            scale, C, S, d, r, k, y + (size_t)g * d, ig,
+                            shat_out ? shat_out + (size_t)g * S : NULL, NULL);
+      if (ig)
+        for (int i = keff; i < k; ++i) ig[i] = -1;
+    }
+    return keff;
+  }
+  /* mode 1: s_hat[t] = max_g s_g[t], g ascending from -inf */
+  float *qlab = (float *)malloc(sizeof(float) * (size_t)r);
+  float *sg = (float *)malloc(sizeof(float) * (size_t)(S > 0 ? S : 1));
+  float *shat = (float *)malloc(sizeof(float) * (size_t)(S > 0 ? S : 1));
+  int32_t *idx = (int32_t *)malloc(sizeof(int32_t) * (size_t)(S > 0 ? S : 1));
+  for (int t = 0; t < S; ++t) shat[t] = -INFINITY;
+  for (int g = 0; g < G; ++g) {
+    oracle_query_label(q_sel + (size_t)g * d, 1, d, C, r, qlab);  /* line 1, head g */
+    if (scale)                                                     /* line 2, head g */
+      oracle_approx_scores_q4(qlab, codes, scale, S, r, sg);
+    else
+      oracle_approx_scores(qlab, L, S, r, sg);
+    for (int t = 0; t < S; ++t) shat[t] = fmaxf(shat[t], sg[t]);
+  }
+  keff = oracle_argtopk(shat, S, k, idx, NULL);                   /* line 3 */
+  for (int g = 0; g < G; ++g)                                     /* lines 4-5 */
+    oracle_attend(q_attn + (size_t)g * d, K, V, d, idx, keff, y + (size_t)g * d);
+  if (idx_out) memcpy(idx_out, idx, sizeof(int32_t) * (size_t)keff);
+  if (shat_out) memcpy(shat_out, shat, sizeof(float) * (size_t)S);
+  free(qlab);
+  free(sg);
+  free(shat);
+  free(idx);
+  return keff;
+}
+
 /* ------------------------------------------------------------------ */
 /* Batched driver over units (b, h): dense tensors
  *   q [B][Hq][d], K,V [B][Hkv][Smax][d], L [B][Hkv][Smax][r],
