@@ -80,6 +80,22 @@ typedef enum { DS_FP16 = 0, DS_BF16 = 1, DS_FP32 = 2 } ds_dtype;
  *                    native label (a bit copy of those channels). */
 typedef enum { DS_LABEL_NATIVE = 0, DS_LABEL_INT4 = 1, DS_LABEL_NONE = 2 } ds_label_format;
 
+/* GQA selection granularity (the paper runs GQA models, Table 3 P:308-310,
+ * without saying how a KV head's G query heads share the selection):
+ *   DS_GROUP_SUM     : reading R3 (default) -- one top-k set per (b, KV
+ *                      head), scored with the group-summed query label
+ *                      Q_label[j] = sum_g q_g[C[j]] (g ascending, fp32).
+ *   DS_GROUP_MAX     : reading R17 -- one set per (b, KV head), scored with
+ *                      max_g of the per-head scores s_g[t] (each the fp32 fma
+ *                      chain of q_g[C[j]] * L[t][j]).  Needs G * r <= 256.
+ *   DS_GROUP_PER_HEAD: reading R17 -- one set per (b, query head): every
+ *                      query head runs Algorithm 1 on its KV head's label and
+ *                      K/V (the layer treated as MHA over shared K/V);
+ *                      topk_idx_out is then [batch][num_q_heads][k].
+ * MAX and PER_HEAD run on 16-bit caches only (fp32 -> DS_ERR_UNSUPPORTED);
+ * PER_HEAD has no prefetch (DS_ERR_UNSUPPORTED) nor ds_approx_scores. */
+typedef enum { DS_GROUP_SUM = 0, DS_GROUP_MAX = 1, DS_GROUP_PER_HEAD = 2 } ds_group_reduce;
+
 /* Outlier-channel modes of Table 3: qk (default), q, k, random. */
 typedef enum { DS_CALIB_QK = 0, DS_CALIB_Q = 1, DS_CALIB_K = 2, DS_CALIB_RANDOM = 3 } ds_calib_mode;
 
@@ -97,7 +113,8 @@ typedef enum { DS_CALIB_QK = 0, DS_CALIB_Q = 1, DS_CALIB_K = 2, DS_CALIB_RANDOM 
  *   label_format   : ds_label_format (0 = native: a zero-initialised
  *                    struct keeps the 16-bit label)
  *   label_scale    : DS_LABEL_INT4 only: dtype [batch][num_kv_heads][max_seq_len],
- *                    16-B aligned; ignored (may be NULL) for native labels. */
+ *                    16-B aligned; ignored (may be NULL) for native labels.
+ *   group_reduce   : ds_group_reduce (0 = DS_GROUP_SUM, reading R3). */
 typedef struct {
   int32_t batch, num_q_heads, num_kv_heads, head_dim;
   int32_t page_size, num_pages, max_pages_per_seq, max_seq_len, r;
@@ -109,6 +126,7 @@ typedef struct {
   const int32_t *channel_idx;
   ds_label_format label_format;
   void *label_scale;
+  ds_group_reduce group_reduce;
 } ds_cache;
 
 /* Human-readable name of a status code (static string, never NULL). */
@@ -162,7 +180,8 @@ size_t ds_decode_workspace_size(const ds_cache *c, int32_t k);
  *   5  y       <- s . V_[i,:]          -> out, rounded to dtype (RNE)
  *   q   : [batch][num_q_heads][head_dim]
  *   out : [batch][num_q_heads][head_dim]
- *   topk_idx_out : nullable int32 [batch][num_kv_heads][k]; positions
+ *   topk_idx_out : nullable int32 [batch][num_kv_heads][k] ([batch][num_q_heads][k]
+ *                  for DS_GROUP_PER_HEAD); positions
  *                  >= k_eff are set to -1.
  *   workspace    : >= ds_decode_workspace_size(c, k) bytes of device memory,
  *                  16-byte aligned, ZERO-FILLED before its first use; every

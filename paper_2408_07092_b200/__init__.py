@@ -24,6 +24,8 @@ DS_FP16, DS_BF16, DS_FP32 = 0, 1, 2
 DS_CALIB_QK, DS_CALIB_Q, DS_CALIB_K, DS_CALIB_RANDOM = 0, 1, 2, 3
 DS_LABEL_NATIVE, DS_LABEL_INT4, DS_LABEL_NONE = 0, 1, 2
 _LF = {"native": DS_LABEL_NATIVE, "int4": DS_LABEL_INT4, "none": DS_LABEL_NONE}
+DS_GROUP_SUM, DS_GROUP_MAX, DS_GROUP_PER_HEAD = 0, 1, 2
+_GR = {"sum": DS_GROUP_SUM, "max": DS_GROUP_MAX, "per_head": DS_GROUP_PER_HEAD}
 
 _DT = {torch.float16: DS_FP16, torch.bfloat16: DS_BF16, torch.float32: DS_FP32}
 
@@ -47,7 +49,8 @@ class ds_cache(ctypes.Structure):
                 ("k_pool", ctypes.c_void_p), ("v_pool", ctypes.c_void_p),
                 ("block_table", ctypes.c_void_p), ("seq_lens", ctypes.c_void_p),
                 ("label", ctypes.c_void_p), ("channel_idx", ctypes.c_void_p),
-                ("label_format", ctypes.c_int), ("label_scale", ctypes.c_void_p)]
+                ("label_format", ctypes.c_int), ("label_scale", ctypes.c_void_p),
+                ("group_reduce", ctypes.c_int)]
 
 
 _lib = None
@@ -145,17 +148,19 @@ class LayerCache:
     channel_idx: torch.Tensor
     label_format: int = DS_LABEL_NATIVE
     label_scale: torch.Tensor | None = None
+    group_reduce: int = DS_GROUP_SUM
 
     @staticmethod
     def allocate(batch, num_q_heads, num_kv_heads, head_dim, max_seq_len, r, dtype, block_table,
                  num_pages=None, page_size=16, device="cuda", channel_idx=None, host_kv=False,
-                 label_format="native"):
+                 label_format="native", group_reduce="sum"):
         """host_kv: K/V pools in pinned host memory (Double Sparsity-Offload,
         P:192): the kernels read them over the host link; label stays on device.
         label_format: "native" (label in K's dtype), "int4" (packed 4-bit
         codes uint8 [B][Hkv][S][ceil(r/2)] + a per-token scale [B][Hkv][S],
         P:171) or "none" (no label cache, the Table 4 ablation); ds.h
-        ds_label_format."""
+        ds_label_format.  group_reduce: "sum" (reading R3), "max" or
+        "per_head" (ds.h ds_group_reduce)."""
         bt = torch.as_tensor(block_table, dtype=torch.int32).to(device).contiguous()
         npages = int(num_pages if num_pages is not None else int(bt.max()) + 1)
         pool = (npages, num_kv_heads, page_size, head_dim)
@@ -180,7 +185,7 @@ class LayerCache:
             bt, torch.zeros(batch, dtype=torch.int32, device=device), label,
             (torch.as_tensor(channel_idx, dtype=torch.int32).to(device).contiguous() if channel_idx is not None
              else torch.zeros((num_kv_heads, r), dtype=torch.int32, device=device)),
-            lf, scale)
+            lf, scale, _GR[group_reduce] if isinstance(group_reduce, str) else int(group_reduce))
 
     @property
     def num_pages(self):
@@ -191,7 +196,7 @@ class LayerCache:
                         self.num_pages, self.block_table.shape[1], self.max_seq_len, self.r,
                         _DT[self.dtype], _ptr(self.k_pool), _ptr(self.v_pool), _ptr(self.block_table),
                         _ptr(self.seq_lens), _ptr(self.label), _ptr(self.channel_idx), self.label_format,
-                        _ptr(self.label_scale))
+                        _ptr(self.label_scale), self.group_reduce)
 
     @property
     def label_bytes(self) -> int:

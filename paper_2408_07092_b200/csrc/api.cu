@@ -30,6 +30,7 @@ CacheView make_view(const ds_cache *c) {
   v.C = c->channel_idx;
   v.lq4 = c->label_format == DS_LABEL_INT4;
   v.lnone = c->label_format == DS_LABEL_NONE;
+  v.greduce = (int)c->group_reduce;
   v.rb = (c->r + 1) / 2;
   v.label_scale = c->label_scale;
   return v;
@@ -75,6 +76,10 @@ static ds_status validate_cache(const ds_cache *c) {
   if ((long long)c->num_pages * c->num_kv_heads * c->page_size >= (1ll << 31)) return DS_ERR_UNSUPPORTED;
   if (c->label_format != DS_LABEL_NATIVE && c->label_format != DS_LABEL_INT4 && c->label_format != DS_LABEL_NONE)
     return DS_ERR_INVALID_ARGUMENT;
+  if (c->group_reduce != DS_GROUP_SUM && c->group_reduce != DS_GROUP_MAX && c->group_reduce != DS_GROUP_PER_HEAD)
+    return DS_ERR_INVALID_ARGUMENT;
+  if (c->group_reduce != DS_GROUP_SUM && c->dtype == DS_FP32) return DS_ERR_UNSUPPORTED;
+  if (c->group_reduce == DS_GROUP_MAX && (c->num_q_heads / c->num_kv_heads) * c->r > 256) return DS_ERR_UNSUPPORTED;
   const bool lab = c->label_format != DS_LABEL_NONE;
   if (!c->k_pool || !c->v_pool || !c->block_table || !c->seq_lens || (lab && !c->label) || !c->channel_idx)
     return DS_ERR_INVALID_ARGUMENT;
@@ -192,6 +197,7 @@ ds_status ds_decode_attention(const ds_cache *c, const void *q, int32_t k, void 
 ds_status ds_approx_scores(const ds_cache *c, const void *q, float *scores_out, cudaStream_t stream) {
   ds_status s = validate_cache(c);
   if (s != DS_OK) return s;
+  if (c->group_reduce == DS_GROUP_PER_HEAD) return DS_ERR_UNSUPPORTED;
   if (!q || !scores_out || !aligned16(q)) return DS_ERR_INVALID_ARGUMENT;
   SelectGeom sg = select_geom(c);
   ScoreParams sc;
@@ -221,7 +227,7 @@ ds_status ds_prefetch_next_layer(const ds_cache *next, const void *q_pred, int32
   if (!q_pred || !aligned16(q_pred)) return DS_ERR_INVALID_ARGUMENT;
   if ((s = check_slot(next, slot)) != DS_OK) return s;
   if (k != slot->k) return DS_ERR_INVALID_ARGUMENT;
-  if (!fused_applicable(next)) return DS_ERR_UNSUPPORTED;
+  if (!fused_applicable(next) || next->group_reduce == DS_GROUP_PER_HEAD) return DS_ERR_UNSUPPORTED;
   FusedParams fp;
   fp.c = make_view(next);
   fp.q = q_pred;

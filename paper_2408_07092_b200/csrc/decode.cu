@@ -159,9 +159,15 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     else return ptr;
   };
   const CacheView &c = p.c;
+  // a unit is one (b, KV head) -- or one (b, query head) for DS_GROUP_PER_HEAD
+  // (reading R17: each query head selects on its own over its KV head's data)
+  const bool perh = c.greduce == DS_GROUP_PER_HEAD;
   const int unit = blockIdx.y;
-  const int b = unit / c.Hkv, h = unit - (unit / c.Hkv) * c.Hkv;
-  const int G = c.G;
+  const int nuh = perh ? c.Hq : c.Hkv;  // units per sequence
+  const int b = unit / nuh, hu = unit - (unit / nuh) * nuh;
+  const int h = perh ? hu / c.G : hu;    // the KV head
+  const int G = perh ? 1 : c.G;          // query heads this unit serves
+  const int hq0 = perh ? hu : h * c.G;   // the first of them
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   DS_TRACE_AT(1, 0);
   if (CL && tid == 0) {
@@ -189,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   // pv[0..1], their scales in pv[2])
   uint4 pv[U];
   bool pre = false;
-  if (c.lnone) {
+  if (c.lnone || c.greduce == DS_GROUP_MAX) {
   } else if (!c.lq4) {
     if constexpr (kVec16) {
       pre = tid + (U - 1) * kThreads < maxloc;
@@ -212,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   const int n = c.seq_lens[b];
   const int keff = min(p.k, n);
   const int nloc = max(0, min(p.chunk, n - t0));
-  T *outp = (T *)p.out + ((size_t)b * c.Hq + (size_t)h * G) * D;
+  T *outp = (T *)p.out + ((size_t)b * c.Hq + (size_t)hq0) * D;
   int32_t *idx = p.idx ? p.idx + (size_t)unit * p.k : nullptr;
   if (n <= 0) {  // empty sequence: y = 0, nothing selected (uniform over the cluster)
     if (crank == 0) {
@@ -226,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
 
   // ---- a1, query tile, zeroing (the tile and C are loaded together; q_lab
   // is then summed from the tile in shared memory)
-  const T *qb = (const T *)p.q + ((size_t)b * c.Hq + (size_t)h * G) * D;
+  const T *qb = (const T *)p.q + ((size_t)b * c.Hq + (size_t)hq0) * D;
   const int r = R > 0 ? R : c.r;
   int chj = 0;
   if (tid < r) chj = c.C[(size_t)h * c.r + tid];
@@ -252,12 +258,22 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   if (btc_ok)
     for (int i = tid; i < npg; i += kThreads) btc[i] = __ldg(c.block_table + (size_t)b * c.maxp + pg0 + i);
   __syncthreads();
-  for (int j = tid; j < r; j += kThreads) {  // Q_label[j] = sum_g q[g][C[j]], g ascending (R3)
-    const int ch = j == tid ? chj : c.C[(size_t)h * c.r + j];
-    float s = 0.0f;
-    for (int g = 0; g < G; ++g)
-      s = s + Elem<T>::to_f(*reinterpret_cast<const T *>(sh.qt + g * ROWB + swz(g, ch >> 3) + (ch & 7) * 2));
-    sh.qlab[j] = s;
+  auto qtile = [&](int g, int ch) {  // q[g][ch] from the swizzled tile
+    return Elem<T>::to_f(*reinterpret_cast<const T *>(sh.qt + g * ROWB + swz(g, ch >> 3) + (ch & 7) * 2));
+  };
+  const bool gmax = c.greduce == DS_GROUP_MAX;
+  if (gmax) {  // R17: per-head query labels q_g[C[j]] at qlab[g * r + j]
+    for (int i = tid; i < G * r; i += kThreads) {
+      const int g = i / r, j = i - (i / r) * r;
+      sh.qlab[i] = qtile(g, c.C[(size_t)h * c.r + j]);
+    }
+  } else {
+    for (int j = tid; j < r; j += kThreads) {  // Q_label[j] = sum_g q[g][C[j]], g ascending (R3)
+      const int ch = j == tid ? chj : c.C[(size_t)h * c.r + j];
+      float s = 0.0f;
+      for (int g = 0; g < G; ++g) s = s + qtile(g, ch);
+      sh.qlab[j] = s;
+    }
   }
   __syncthreads();
   float ql[R > 0 ? R : 1];
@@ -269,17 +285,39 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
 
   DS_TRACE_AT(1, 12);
   // ---- a2: stream this CTA's label rows -> order keys + digit-1 histogram
-  if (c.lnone) {
+  const T *kp = (const T *)c.k_pool;
+  const int32_t *btb = c.block_table + (size_t)b * c.maxp;
+  auto krow = [&](int t) -> const T * {  // token t's paged K row (DS_LABEL_NONE)
+    const int pg = t / c.P;
+    const int32_t page = btc_ok ? btc[pg - pg0] : __ldg(btb + pg);
+    return kp + (((size_t)page * c.Hkv + h) * c.P + (t - pg * c.P)) * (size_t)D;
+  };
+  if (gmax) {
+    // R17: s_hat[t] = max_g (fma chain of q_g[C[j]] * L[t][j]) -- a plain
+    // loop (diagnostic variant), every label format
+    for (int i = tid; i < nloc; i += kThreads) {
+      const T *kr = c.lnone ? krow(t0 + i) : nullptr;
+      float m = -INFINITY;
+      for (int g = 0; g < G; ++g) {
+        const float *qv = sh.qlab + g * r;
+        float s;
+        if (c.lq4) {
+          s = q4_score<T>(cod + (size_t)i * c.rb, scl[i], qv, r);
+        } else {
+          s = 0.0f;
+          for (int j = 0; j < r; ++j)
+            s = fmaf(qv[j], Elem<T>::to_f(c.lnone ? kr[c.C[(size_t)h * c.r + j]] : lab[(size_t)i * r + j]), s);
+        }
+        m = fmaxf(m, s);
+      }
+      const uint32_t k0 = order_key(m);
+      keys[i] = k0;
+      DS_HIST_ADD(&sh.h1[k0 >> kSh1]);
+    }
+  } else if (c.lnone) {
     // no label cache (the Table 4 ablation): the r channels are
     // read straight from each token's paged K row -- 2-byte reads scattered
     // over the 256-B row, one DRAM sector or more per channel
-    const T *kp = (const T *)c.k_pool;
-    const int32_t *bt = c.block_table + (size_t)b * c.maxp;
-    auto krow = [&](int t) -> const T * {
-      const int pg = t / c.P;
-      const int32_t page = btc_ok ? btc[pg - pg0] : __ldg(bt + pg);
-      return kp + (((size_t)page * c.Hkv + h) * c.P + (t - pg * c.P)) * (size_t)D;
-    };
     int i0 = tid;
     if constexpr (R > 0) {
       int chs[R];
@@ -1119,7 +1157,7 @@ static cudaError_t launch_cl(const ds_cache *c, const FusedParams &p, int nch, c
   if (attr != cudaSuccess) return attr;
   if (smem > (size_t)kFusedMaxSmem) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nch, c->batch * c->num_kv_heads);
+  cfg.gridDim = dim3(nch, c->batch * (c->group_reduce == DS_GROUP_PER_HEAD ? c->num_q_heads : c->num_kv_heads));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -1148,7 +1186,7 @@ int fused_cluster(const ds_cache *c) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int units = c->batch * c->num_kv_heads;
+  const int units = c->batch * (c->group_reduce == DS_GROUP_PER_HEAD ? c->num_q_heads : c->num_kv_heads);
   int nch = units * 4 >= sms * 3 ? 1 : sms / units;
   if (nch > 8) nch = 8;
   const int need = (c->max_seq_len + fused::kMaxS - 1) / fused::kMaxS;

@@ -16,6 +16,7 @@ struct CacheView {
   const int32_t *C;
   int lq4, rb;              // DS_LABEL_INT4; code bytes per label row (ceil(r/2))
   int lnone;                // DS_LABEL_NONE: line 2 reads the channels from the K pool
+  int greduce;              // ds_group_reduce
   const void *label_scale;  // DS_LABEL_INT4: [B][Hkv][Smax] of the cache dtype
 };
 

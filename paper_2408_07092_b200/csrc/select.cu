@@ -163,12 +163,16 @@ __global__ void __launch_bounds__(kThreads, 2) score_select_kernel(ScoreParams p
   const int npg = nloc > 0 ? (t0 + nloc - 1) / c.P - pg0 + 1 : 0;
   if (!p.scores && bt_cached)
     for (int i = tid; i < npg; i += kThreads) btrow[i] = __ldg(bt + pg0 + i);
-  for (int j = tid; j < r; j += kThreads) {
+  const bool gmax = c.greduce == DS_GROUP_MAX;  // R17 (host-checked: G * r <= kMaxR)
+  for (int i = tid; i < (gmax ? c.G * r : r); i += kThreads) {
     const T *qb = (const T *)p.q + ((size_t)b * c.Hq + (size_t)h * c.G) * c.D;
+    const int g0 = gmax ? i / r : 0, j = gmax ? i - g0 * r : i;
     const int ch = c.C[(size_t)h * c.r + j];
     float s = 0.0f;
-    for (int g = 0; g < c.G; ++g) s = s + Elem<T>::to_f(qb[(size_t)g * c.D + ch]);
-    sh.qlab[j] = s;
+    if (gmax) s = Elem<T>::to_f(qb[(size_t)g0 * c.D + ch]);  // per-head label q_g[C[j]]
+    else
+      for (int g = 0; g < c.G; ++g) s = s + Elem<T>::to_f(qb[(size_t)g * c.D + ch]);
+    sh.qlab[i] = s;
   }
   for (int i = tid; i < kD1; i += kThreads) sh.h1[i] = 0;
   for (int i = tid; i < kD2; i += kThreads) sh.h2[i] = 0;
@@ -189,16 +193,22 @@ __global__ void __launch_bounds__(kThreads, 2) score_select_kernel(ScoreParams p
   const T *lab = (const T *)c.label + lrow * (size_t)c.r;
   const uint8_t *cod = (const uint8_t *)c.label + lrow * (size_t)c.rb;  // 4-bit label (R16)
   const T *scl = (const T *)c.label_scale + lrow;
-  auto score_at = [&](int i) {
+  auto head_score = [&](int i, const float *qv) {
     if (c.lnone) {  // no label cache (Table 4 ablation): the channels of the paged K row
       const int t = t0 + i;
       const T *kr = (const T *)c.k_pool +
                     (((size_t)__ldg(bt + t / c.P) * c.Hkv + h) * c.P + t % c.P) * (size_t)c.D;
       float s = 0.0f;
-      for (int j = 0; j < r; ++j) s = fmaf(qs[j], Elem<T>::to_f(kr[c.C[(size_t)h * c.r + j]]), s);
+      for (int j = 0; j < r; ++j) s = fmaf(qv[j], Elem<T>::to_f(kr[c.C[(size_t)h * c.r + j]]), s);
       return s;
     }
-    return c.lq4 ? q4_score<T>(cod + (size_t)i * c.rb, scl[i], qs, r) : label_score<T, R>(lab + (size_t)i * r, qs, r);
+    return c.lq4 ? q4_score<T>(cod + (size_t)i * c.rb, scl[i], qv, r) : label_score<T, R>(lab + (size_t)i * r, qv, r);
+  };
+  auto score_at = [&](int i) {
+    if (!gmax) return head_score(i, qs);
+    float m = -INFINITY;  // R17: max over the group's per-head scores
+    for (int g = 0; g < c.G; ++g) m = fmaxf(m, head_score(i, sh.qlab + g * r));
+    return m;
   };
   if (p.scores) {  // diagnostics entry (ds_approx_scores): s_hat to HBM
     float *so = p.scores + (size_t)unit * c.Smax + t0;
@@ -209,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 2) score_select_kernel(ScoreParams p
   int i0 = tid;
   if constexpr (R > 0 && R * sizeof(T) == 16) {
     constexpr int U = kUnroll;
-    for (; !c.lq4 && !c.lnone && i0 + (U - 1) * kThreads < nloc; i0 += U * kThreads) {
+    for (; !c.lq4 && !c.lnone && !gmax && i0 + (U - 1) * kThreads < nloc; i0 += U * kThreads) {
       uint4 v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = __ldg(reinterpret_cast<const uint4 *>(lab) + (size_t)(i0 + u * kThreads));

@@ -114,5 +114,5 @@ def test_ds_cache_struct_layout_matches_header():
     body = body[:body.index("} ds_cache;")]
     decl = re.findall(r"\*?\s*(\w+)\s*[,;]", body)   # declarators in order
     assert decl == names
-    assert names[-2:] == ["label_format", "label_scale"]
+    assert names[-3:] == ["label_format", "label_scale", "group_reduce"]
     assert ds.ds_cache().label_format == ds.DS_LABEL_NATIVE
