@@ -494,19 +494,28 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     } else {
       const int gcmp = whole1 ? (int)D1 - 1 : (int)D1;
       const uint32_t ecmp = whole1 ? 0xffffffffu : D1;
-      for (int base = w0; base < w1; base += 128) {
-        uint32_t kk[4];
+      // rounds of 32 groups: every key load of a round is in flight at once,
+      // lane l keeps group l's two masks and stores them once
+      const int g1 = (w1 + 31) >> 5;
+      for (int gb0 = w0 >> 5; gb0 < g1; gb0 += 32) {
+        uint32_t kk[32];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) kk[e] = keys[base + 32 * e + lane];
+        for (int e = 0; e < 32; ++e) {
+          const int i = (gb0 + e) * 32 + lane;
+          kk[e] = i < w1 ? keys[i] : 0u;
+        }
+        uint32_t mym = 0u, mye = 0u;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
+        for (int e = 0; e < 32; ++e) {
           const uint32_t d = kk[e] >> kSh1;
           const uint32_t mg = __ballot_sync(0xffffffffu, (int)d > gcmp);
           const uint32_t me = __ballot_sync(0xffffffffu, d == ecmp);
-          if (lane == e) {
-            sh.gtm[(base >> 5) + e] = mg;
-            sh.eqm[(base >> 5) + e] = me;
-          }
+          mym = lane == e ? mg : mym;
+          mye = lane == e ? me : mye;
+        }
+        if (gb0 + lane < g1) {
+          sh.gtm[gb0 + lane] = mym;
+          sh.eqm[gb0 + lane] = mye;
         }
       }
       __syncwarp();
