@@ -494,28 +494,19 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     } else {
       const int gcmp = whole1 ? (int)D1 - 1 : (int)D1;
       const uint32_t ecmp = whole1 ? 0xffffffffu : D1;
-      // rounds of 32 groups: every key load of a round is in flight at once,
-      // lane l keeps group l's two masks and stores them once
-      const int g1 = (w1 + 31) >> 5;
-      for (int gb0 = w0 >> 5; gb0 < g1; gb0 += 32) {
-        uint32_t kk[32];
+      for (int base = w0; base < w1; base += 128) {
+        uint32_t kk[4];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int i = (gb0 + e) * 32 + lane;
-          kk[e] = i < w1 ? keys[i] : 0u;
-        }
-        uint32_t mym = 0u, mye = 0u;
+        for (int e = 0; e < 4; ++e) kk[e] = keys[base + 32 * e + lane];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
+        for (int e = 0; e < 4; ++e) {
           const uint32_t d = kk[e] >> kSh1;
           const uint32_t mg = __ballot_sync(0xffffffffu, (int)d > gcmp);
           const uint32_t me = __ballot_sync(0xffffffffu, d == ecmp);
-          mym = lane == e ? mg : mym;
-          mye = lane == e ? me : mye;
-        }
-        if (gb0 + lane < g1) {
-          sh.gtm[gb0 + lane] = mym;
-          sh.eqm[gb0 + lane] = mye;
+          if (lane == e) {
+            sh.gtm[(base >> 5) + e] = mg;
+            sh.eqm[(base >> 5) + e] = me;
+          }
         }
       }
       __syncwarp();
@@ -611,6 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     };
     if (tail) {
       boundary1024(sh.h2, sh.c2, need1, sh.state + 3, 0);
+      DS_TRACE_BY(1, 14, kAttThreads);
       const uint32_t P2 = (D1 << (kSh1 - kSh2)) | sh.state[3];
       const uint32_t need2 = need1 - sh.state[4];
       const uint32_t cnt2 = sh.state[5];
@@ -626,14 +618,27 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         // the cluster's members land in h2 (no CTA reads it after exchange 1)
         uint2 *gathered = reinterpret_cast<uint2 *>(sh.h2);
         static_assert(sizeof(sh.h2) >= kMaxMembers * sizeof(uint2), "member buffer");
-        uint32_t off = 0;
-        for (int cr = 0; cr < nch; ++cr) {
-          const uint32_t m = remote(&sh.nmem, cr)[0];
-          const uint2 *rm = remote(sh.members, cr);
-          for (int i = stid; i < (int)m; i += kSelThreads) gathered[off + i] = rm[i];
-          off += m;
+        // every CTA's member count in one round trip (lane cr of warp 0), the
+        // offsets in c2 (free after exchange 1), then every CTA's members in
+        // one pass so the remote reads of all CTAs overlap
+        if (sw == 0) {
+          const uint32_t m = lane < nch ? remote(&sh.nmem, lane)[0] : 0u;
+          uint32_t incl = m;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          sh.c2[lane] = incl - m;  // exclusive offset of CTA lane
         }
         sel_sync();
+        for (int i = stid; i < (int)cnt2; i += kSelThreads) {
+          int cr = 0;
+          for (int j = 1; j < nch; ++j) cr += (uint32_t)i >= sh.c2[j] ? 1 : 0;
+          gathered[i] = remote(sh.members, cr)[i - (int)sh.c2[cr]];
+        }
+        sel_sync();
+        DS_TRACE_BY(1, 15, kAttThreads);
         const int nm = (int)cnt2;  // rank by (key desc, token asc)
         for (int i = stid; i < nm; i += kSelThreads) {
           const uint2 me = gathered[i];

@@ -3,6 +3,7 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/gather_bw scripts/gather_bw.cu
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 #include <random>
 #include <algorithm>
@@ -17,7 +18,7 @@ __device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\
 // each warp: rows [w*per, (w+1)*per) of its CTA's list; batch of 8 rows (K and V = 16 rows of 256 B)
 template <int STAGES>
 __global__ void gather(const uint8_t *kp, const uint8_t *vp, const uint32_t *rows, int rows_per_cta, int warps,
-                       unsigned long long *sink) {
+                       unsigned long long *sink, int stride) {
   extern __shared__ __align__(128) uint8_t sm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (w >= warps) return;
@@ -31,7 +32,7 @@ __global__ void gather(const uint8_t *kp, const uint8_t *vp, const uint32_t *row
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
       const int q = lane + 32 * m, rr = q >> 4, ch = q & 15;
-      const size_t off = (size_t)lst[lo + j * 8 + rr] * 256 + ch * 16;
+      const size_t off = (size_t)lst[lo + j * 8 + rr] * stride + ch * 16;
       const uint32_t dst = (uint32_t)__cvta_generic_to_shared(st + rr * 256 + ch * 16);
       cp16(dst, kp + off);
       cp16(dst + 2048, vp + off);
@@ -64,8 +65,16 @@ int main() {
   const size_t pages = units / Hkv * (S / P);   // B * S/P pages, each [Hkv][P][256 B]
   const size_t pool_rows = pages * Hkv * P;
   uint8_t *kp, *vp; uint32_t *rows; unsigned long long *sink;
-  cudaMalloc(&kp, pool_rows * 256); cudaMalloc(&vp, pool_rows * 256);
-  cudaMemset(kp, 1, pool_rows * 256); cudaMemset(vp, 1, pool_rows * 256);
+  // INTERLEAVE=1: K and V rows of a token adjacent (one 512-B row), else two pools of 256-B rows
+  const int inter = getenv("INTERLEAVE") && atoi(getenv("INTERLEAVE"));
+  const int stride = inter ? 512 : 256;
+  if (inter) {
+    cudaMalloc(&kp, pool_rows * 512); cudaMemset(kp, 1, pool_rows * 512); vp = kp + 256;
+  } else {
+    cudaMalloc(&kp, pool_rows * 256); cudaMalloc(&vp, pool_rows * 256);
+    cudaMemset(kp, 1, pool_rows * 256); cudaMemset(vp, 1, pool_rows * 256);
+  }
+  printf("layout: %s\n", inter ? "interleaved K|V 512-B rows" : "separate K and V pools, 256-B rows");
   cudaMalloc(&sink, 8);
   std::mt19937_64 g(1);
   // per unit: k random distinct tokens, random page permutation -> pool rows
@@ -94,7 +103,7 @@ int main() {
     for (int it = 0; it < 5; ++it) {
       flush_read<<<592, 512>>>((const uint4 *)fl, (512u << 20) / 16, sink);
       cudaEventRecord(e0);
-      kern<<<ctas, warps * 32, smem>>>(kp, vp, rows, rpc, warps, sink);
+      kern<<<ctas, warps * 32, smem>>>(kp, vp, rows, rpc, warps, sink, stride);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
