@@ -34,6 +34,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "ds_common.cuh"
 #include "ds_internal.h"
@@ -1203,7 +1204,17 @@ int fused_cluster(const ds_cache *c) {
   const int units = c->batch * (c->group_reduce == DS_GROUP_PER_HEAD ? c->num_q_heads : c->num_kv_heads);
   int nch = units * 4 >= sms * 3 ? 1 : sms / units;
   if (nch > 8) nch = 8;
+  // short sequences: a cluster's fixed exchange cost (~4-5 us) outweighs the
+  // split streaming/gather time (measured on c2, B=1 MHA: S=4K one CTA per
+  // unit 15.9 us vs 18.1 us for a cluster of 4; S=16K even; S=32K 4 CTAs win)
+  if (c->max_seq_len <= 8192) nch = 1;
   const int need = (c->max_seq_len + fused::kMaxS - 1) / fused::kMaxS;
+#ifdef DS_EXP_NCH_ENV  // timing experiments only (never in libds.so): DS_NCH forces the cluster size
+  if (const char *e = getenv("DS_NCH")) {
+    const int v = atoi(e);
+    if (v >= need && v >= 1 && v <= 16) return v;
+  }
+#endif
   if (nch < need) nch = need;
   if (nch < 1) nch = 1;
   return nch;

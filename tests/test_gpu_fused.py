@@ -55,7 +55,7 @@ CASES = [
     ("k1_bf16", synth.Config("k1", B=16, Hq=32, Hkv=8, d=128, S=1024, r=8, k=1, dtype="bf16"), 1, "iid"),
     ("kS_bf16", synth.Config("kS", B=16, Hq=32, Hkv=8, d=128, S=700, r=8, k=700, dtype="bf16"), 700, "iid"),
     # few units -> a cluster of CTAs per unit (DSMEM histograms, cluster merge)
-    ("cl4_mha_fp16", synth.Config("c4u", B=4, Hq=32, Hkv=8, d=128, S=6000, r=8, k=375, dtype="fp16"), 375, "iid"),
+    ("cl4_mha_fp16", synth.Config("c4u", B=4, Hq=32, Hkv=8, d=128, S=9000, r=8, k=375, dtype="fp16"), 375, "iid"),
     ("cl8_gqa_bf16_d64", synth.Config("c8u", B=4, Hq=8, Hkv=2, d=64, S=9000, r=4, k=500, dtype="bf16",
                                       page_size=7), 500, "clustered"),
 ]

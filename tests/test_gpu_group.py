@@ -58,8 +58,8 @@ def check(lay, cache, group, k, y, idx, units):
 
 CASES = [
     ("gqa4_bf16", synth.Config("g4", B=16, Hq=32, Hkv=8, d=128, S=2048, r=8, k=128, dtype="bf16"), "native", None),
-    ("cl_gqa8_fp16", synth.Config("g8", B=2, Hq=16, Hkv=2, d=128, S=5000, r=8, k=300, dtype="fp16"), "native",
-     [5000, 2222]),
+    ("cl_gqa8_fp16", synth.Config("g8", B=2, Hq=16, Hkv=2, d=128, S=10000, r=8, k=300, dtype="fp16"), "native",
+     [10000, 2222]),
     ("gqa2_int4_d64", synth.Config("g2", B=4, Hq=8, Hkv=4, d=64, S=3000, r=4, k=200, dtype="bf16"), "int4",
      [3000, 1, 0, 1500]),
     ("gqa4_nolabel", synth.Config("gn", B=4, Hq=16, Hkv=4, d=128, S=2500, r=8, k=150, dtype="bf16"), "none", None),

@@ -16,8 +16,8 @@ pytestmark = pytest.mark.gpu
 
 CASES = [
     ("gqa4_bf16", synth.Config("n4a", B=16, Hq=32, Hkv=8, d=128, S=2048, r=8, k=128, dtype="bf16"), None),
-    ("cl_mha_fp16", synth.Config("n4b", B=4, Hq=32, Hkv=8, d=128, S=6000, r=8, k=375, dtype="fp16"),
-     [6000, 3001, 1, 0]),
+    ("cl_mha_fp16", synth.Config("n4b", B=4, Hq=32, Hkv=8, d=128, S=9000, r=8, k=375, dtype="fp16"),
+     [9000, 3001, 1, 0]),
     ("d64_r4_page7_long", synth.Config("n4c", B=2, Hq=8, Hkv=2, d=64, S=30000, r=4, k=1000, dtype="bf16",
                                        page_size=7), [30000, 12345]),
     ("c1_fp32", synth.CONFIGS["c1"], None),

@@ -124,7 +124,7 @@ DECODE = [
                                      page_size=7), "iid"),
     ("kS_bf16", synth.Config("d4d", B=16, Hq=32, Hkv=8, d=128, S=700, r=8, k=700, dtype="bf16"), "iid"),
     # clusters of CTAs per unit
-    ("cl_mha_fp16", synth.Config("d4e", B=4, Hq=32, Hkv=8, d=128, S=6000, r=8, k=375, dtype="fp16"), "iid"),
+    ("cl_mha_fp16", synth.Config("d4e", B=4, Hq=32, Hkv=8, d=128, S=9000, r=8, k=375, dtype="fp16"), "iid"),
     ("cl_gqa_bf16_d64", synth.Config("d4f", B=4, Hq=8, Hkv=2, d=64, S=9000, r=4, k=500, dtype="bf16",
                                      page_size=7), "clustered"),
     # fp32: the two-kernel path
