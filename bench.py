@@ -3,7 +3,7 @@
 "sparse decode-attn us/layer & HBM GB/s vs dense, S=32K, 1/16 sparsity, 1-8 B200").
 
 A step = one decode step of the whole hot path over L resident layer caches:
-per layer a0 (ds_append_kv of the current token) + a1..a5 (ds_decode_attention).
+per layer a0 (the current token's K/V + label row) + a1..a5, as one ds_decode_attention_append.
 Workload at N=1: c3 (Llama-3-8B GQA, B=16, H_q=32, H_kv=8, d=128, S=32768,
 r=8, k=2048, bf16) -- the config BASELINE.json's metric names (S=32K, 1-8 B200).
 N>1 (torchrun, one rank per GPU): weak scaling, every rank runs its own c3
@@ -277,13 +277,12 @@ def run_ours(args, dist):
     sp = ctypes.c_void_p(stream.cuda_stream)
     P = ctypes.c_void_p
 
-    def step():
+    def step():  # a0 + a1..a5 per layer: ds_decode_attention_append (one launch on the single-kernel path)
         for i, ly in enumerate(layers):
-            ds._check(lib.ds_append_kv(ctypes.byref(ly["cs"]), P(ly["k_new"].data_ptr()), P(ly["v_new"].data_ptr()),
-                                       P(ly["pos"].data_ptr()), 1, sp), "append")
-            ds._check(lib.ds_decode_attention(ctypes.byref(ly["cs"]), P(ly["q"].data_ptr()), k,
-                                              P(ly["out"].data_ptr()), None, P(ws.data_ptr()), ws.numel(), sp),
-                      "decode")
+            ds._check(lib.ds_decode_attention_append(ctypes.byref(ly["cs"]), P(ly["k_new"].data_ptr()),
+                                                     P(ly["v_new"].data_ptr()), P(ly["pos"].data_ptr()),
+                                                     P(ly["q"].data_ptr()), k, P(ly["out"].data_ptr()), None,
+                                                     P(ws.data_ptr()), ws.numel(), sp), "append+decode")
             if gathered is not None:
                 shard.allgather_heads(dist.pg, ly["out"], gathered[i])   # the path's one exchange step
 
@@ -338,7 +337,8 @@ def run_ours(args, dist):
                                   "ds_decode_attention launch group (score_select_kernel + attn_mma_kernel)"),
                        "us_per_launch": round(us_decode, 3), "peak_source": peak_src,
                        "algorithmic_bytes_per_launch": bytes_layer}
-    res["gpu_launches"] = args.steps * L * (KERNELS_PER_APPEND + n_dec)
+    # per layer: 1 fused launch on the single-kernel path, else append + 2 decode kernels
+    res["gpu_launches"] = args.steps * L * (1 if n_dec == 1 else KERNELS_PER_APPEND + n_dec)
     if clocks:
         res["clocks"] = clocks
 
@@ -386,8 +386,8 @@ def e2e(args, dist, layers, ws, k, stream, cfg):
             ly["q"].copy_(hq[i], non_blocking=True)
             ly["k_new"].copy_(hk[i], non_blocking=True)
             ly["v_new"].copy_(hv[i], non_blocking=True)
-            ds.ds_append_kv(ly["cache"], ly["k_new"], ly["v_new"], ly["pos"], cs=ly["cs"])
-            ds.ds_decode_attention(ly["cache"], ly["q"], k, out=ly["out"], ws=ws, cs=ly["cs"])
+            ds.ds_decode_attention_append(ly["cache"], ly["k_new"], ly["v_new"], ly["pos"], ly["q"], k,
+                                          out=ly["out"], ws=ws, cs=ly["cs"])
             ho[i].copy_(ly["out"], non_blocking=True)
 
     with torch.cuda.stream(stream):
@@ -409,7 +409,7 @@ def e2e(args, dist, layers, ws, k, stream, cfg):
     val = ledger.layer_bytes_alg(cfg, args.label) * L * nr / (ms / 1e3) / 1e9 if args.mode == "weak" else \
         ledger.layer_bytes_alg(synth.CONFIGS[args.config], args.label) * L / (ms / 1e3) / 1e9
     return {"value": round(val, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": round(ms, 5), "api": "paper_2408_07092_b200.ds_append_kv + ds_decode_attention (eager)"}
+            "ms_per_step": round(ms, 5), "api": "paper_2408_07092_b200.ds_decode_attention_append (eager)"}
 
 
 def extra_configs(args):

@@ -244,6 +244,24 @@ ds_status ds_prefetch_next_layer(const ds_cache *next, const void *q_pred, int32
 ds_status ds_decode_attention_prefetched(const ds_cache *c, const void *q, const ds_prefetch_slot *slot,
                                          void *out, cudaStream_t stream);
 
+/* One decode step of a layer in one launch: ds_append_kv of one new token
+ * per sequence (n_new = 1; "in the decoding phase, only the heavy
+ * channel values of new tokens are added") followed by ds_decode_attention
+ * (Algorithm 1), with the same results and the same cache contents as the
+ * two calls in sequence.  The caller sets seq_lens[b] to include the new
+ * token (positions[b] < seq_lens[b], reading R10) before the call.
+ *   k_new, v_new : [batch][1][num_kv_heads][head_dim] (device, 16-B aligned)
+ *   positions    : int32 [batch] (device), the new token's position
+ *   q, k, out, topk_idx_out, workspace : as ds_decode_attention.
+ * On the single-kernel path the CTA whose chunk holds the new token writes
+ * its K/V and label rows and scores it from the values it wrote; fp32
+ * caches run the append kernel and then the two-kernel decode.
+ * Errors: as ds_append_kv and ds_decode_attention. */
+ds_status ds_decode_attention_append(const ds_cache *c, const void *k_new, const void *v_new,
+                                     const int32_t *positions, const void *q, int32_t k, void *out,
+                                     int32_t *topk_idx_out, void *workspace, size_t workspace_bytes,
+                                     cudaStream_t stream);
+
 /* Lines 1-2 of Algorithm 1 only, for diagnostics and tests:
  * scores_out fp32 [batch][num_kv_heads][max_seq_len]; entries t >=
  * seq_lens[b] are left untouched.  Same arithmetic as ds_decode_attention. */

@@ -75,6 +75,8 @@ def lib():
         L.ds_decode_workspace_size.restype = SZ
         L.ds_decode_attention.argtypes = [C, P, I32, P, P, P, SZ, P]
         L.ds_approx_scores.argtypes = [C, P, P, P]
+        L.ds_decode_attention_append.argtypes = [C, P, P, P, P, I32, P, P, P, SZ, P]
+        L.ds_decode_attention_append.restype = ctypes.c_int
         SL = ctypes.POINTER(ds_prefetch_slot)
         L.ds_prefetch_next_layer.argtypes = [C, P, I32, SL, P]
         L.ds_decode_attention_prefetched.argtypes = [C, P, SL, P, P]
@@ -95,7 +97,7 @@ def lib():
 EXPORTS = ("ds_status_string", "ds_version", "ds_calibrate_channels", "ds_append_kv",
            "ds_decode_workspace_size", "ds_decode_attention", "ds_approx_scores",
            "ds_dense_workspace_size", "ds_dense_decode_attention", "ds_decode_launches",
-           "ds_prefetch_next_layer", "ds_decode_attention_prefetched")
+           "ds_prefetch_next_layer", "ds_decode_attention_prefetched", "ds_decode_attention_append")
 
 
 def ds_status_string(s: int) -> str:
@@ -251,6 +253,22 @@ def ds_decode_attention(cache: LayerCache, q, k, out=None, topk_idx_out=None, ws
     st = lib().ds_decode_attention(ctypes.byref(cs), _ptr(q), k, _ptr(out), _ptr(topk_idx_out), _ptr(ws),
                                    ws.numel(), _stream(stream))
     _check(st, "ds_decode_attention")
+    return out
+
+
+def ds_decode_attention_append(cache: LayerCache, k_new, v_new, positions, q, k, out=None, topk_idx_out=None,
+                               ws=None, stream=None, cs=None):
+    """One decode step in one launch: ds_append_kv of one token per sequence
+    (k_new, v_new [B][1][Hkv][d], positions [B]) then Algorithm 1.  The
+    caller has already set seq_lens to include the new token."""
+    cs = cs if cs is not None else cache.struct()
+    if out is None:
+        out = torch.empty_like(q)
+    if ws is None:
+        ws = workspace(lib().ds_decode_workspace_size(ctypes.byref(cs), k), q.device)
+    st = lib().ds_decode_attention_append(ctypes.byref(cs), _ptr(k_new), _ptr(v_new), _ptr(positions), _ptr(q), k,
+                                          _ptr(out), _ptr(topk_idx_out), _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "ds_decode_attention_append")
     return out
 
 

@@ -172,6 +172,8 @@ ds_status ds_decode_attention(const ds_cache *c, const void *q, int32_t k, void 
     fp.out = out;
     fp.idx = topk_idx_out;
     fp.select_only = 0;
+    fp.k_new = fp.v_new = nullptr;
+    fp.positions = nullptr;
     fp.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c->head_dim));
     return cuda_status(launch_fused(c, fp, stream));
   }
@@ -192,6 +194,34 @@ ds_status ds_decode_attention(const ds_cache *c, const void *q, int32_t k, void 
   fill_attn(ap, c, q, w.rowid, k, ag, out);
   ap.ready = w.ready;
   return cuda_status(launch_attn(c, ap, ag, stream));
+}
+
+ds_status ds_decode_attention_append(const ds_cache *c, const void *k_new, const void *v_new,
+                                     const int32_t *positions, const void *q, int32_t k, void *out,
+                                     int32_t *topk_idx_out, void *workspace, size_t workspace_bytes,
+                                     cudaStream_t stream) {
+  ds_status s = validate_cache(c);
+  if (s != DS_OK) return s;
+  if (!positions || !k_new || !v_new || !aligned16(k_new) || !aligned16(v_new)) return DS_ERR_INVALID_ARGUMENT;
+  if (k < 1 || k > c->max_seq_len || !q || !out || !aligned16(q) || !aligned16(out)) return DS_ERR_INVALID_ARGUMENT;
+  Workspace w = carve_workspace(c, k, workspace);
+  if (!workspace || workspace_bytes < w.bytes || !aligned16(workspace)) return DS_ERR_WORKSPACE_TOO_SMALL;
+  if (!fused_applicable(c)) {  // fp32: the append kernel, then the two-kernel decode
+    if (launch_append(c, k_new, v_new, positions, 1, stream) != cudaSuccess) return DS_ERR_CUDA;
+    return ds_decode_attention(c, q, k, out, topk_idx_out, workspace, workspace_bytes, stream);
+  }
+  FusedParams fp;
+  fp.c = make_view(c);
+  fp.q = q;
+  fp.k = k;
+  fp.out = out;
+  fp.idx = topk_idx_out;
+  fp.select_only = 0;
+  fp.k_new = k_new;
+  fp.v_new = v_new;
+  fp.positions = positions;
+  fp.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c->head_dim));
+  return cuda_status(launch_fused(c, fp, stream));
 }
 
 ds_status ds_approx_scores(const ds_cache *c, const void *q, float *scores_out, cudaStream_t stream) {
@@ -236,6 +266,8 @@ ds_status ds_prefetch_next_layer(const ds_cache *next, const void *q_pred, int32
   fp.idx = slot->idx;
   fp.scale_log2 = 0.f;
   fp.select_only = 1;
+  fp.k_new = fp.v_new = nullptr;
+  fp.positions = nullptr;
   if (launch_fused(next, fp, side_stream) != cudaSuccess) return DS_ERR_CUDA;
   return cuda_status(launch_gather(next, slot, side_stream));
 }

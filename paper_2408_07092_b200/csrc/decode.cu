@@ -90,6 +90,9 @@ struct alignas(128) Sh {
   uint32_t cnt[4];             // [3] this CTA's selected count (read remotely)
   uint32_t ncand, nmem, lower_sel, pad0;
   uint64_t xbar[4];            // cluster exchange barriers of the selection warps
+  float newlab[kMaxR];         // fused append: the new token's label values (int4: codes)
+  float newscale;              // fused append, int4: its scale
+  int newpos;                  // fused append: the new token's position (-1: none)
   alignas(16) uint8_t qt[8 * 128 * 2];  // query rows (heads >= G zero), 16-B chunks swizzled
 };
 
@@ -184,6 +187,33 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   const T *lab = (const T *)c.label + lrow * (size_t)c.r;
   const uint8_t *cod = (const uint8_t *)c.label + lrow * (size_t)c.rb;  // 4-bit label (R16)
   const T *scl = (const T *)c.label_scale + lrow;
+  // fused append: the CTA whose chunk holds the new token writes its K/V
+  // rows and (16-bit) label row here and keeps its r channel values; after
+  // the stream one thread re-scores it (the stream may have read the old
+  // label row) and writes a 4-bit label row (kept out of this register-tight
+  // prologue).  One writer per KV head in per-head mode.
+  if (p.k_new && warp == 0) {  // before this warp holds the label prefetch
+    const int pn = p.positions[b];
+    if (lane == 0) sh.newpos = pn;
+    if (pn >= t0 && pn < t0 + max(0, min(p.chunk, c.seq_lens[b] - t0))) {
+      const T *kr = (const T *)p.k_new + ((size_t)b * c.Hkv + h) * D;
+      const T *vr = (const T *)p.v_new + ((size_t)b * c.Hkv + h) * D;
+      const int32_t *Ch = c.C + (size_t)h * c.r;
+      if (!perh || hq0 % c.G == 0) {
+        const int page = c.block_table[(size_t)b * c.maxp + pn / c.P];
+        const size_t dst = (((size_t)page * c.Hkv + h) * c.P + (pn % c.P)) * (size_t)D;
+        for (int v = lane; v < 2 * CHN; v += 32) {
+          if (v < CHN) reinterpret_cast<uint4 *>((T *)c.k_pool + dst)[v] = reinterpret_cast<const uint4 *>(kr)[v];
+          else reinterpret_cast<uint4 *>((T *)c.v_pool + dst)[v - CHN] = reinterpret_cast<const uint4 *>(vr)[v - CHN];
+        }
+        if (!c.lq4 && !c.lnone) {
+          T *lab = (T *)c.label + (((size_t)b * c.Hkv + h) * c.Smax + pn) * c.r;
+          for (int j = lane; j < c.r; j += 32) lab[j] = kr[Ch[j]];
+        }
+      }
+      for (int j = lane; j < c.r; j += 32) sh.newlab[j] = Elem<T>::to_f(kr[Ch[j]]);
+    }
+  }
   // The first label batch is requested before anything else waits on memory,
   // so the prologue's round trips (seq_lens, C, q) overlap it.  Its bound is
   // the allocation (Smax), not seq_lens: rows past the sequence are read and
@@ -428,6 +458,46 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   DS_TRACE_AT(1, 13);
   if (tid < 128) keys[nloc + tid] = 0u;  // pad: below every finite score's key
   __syncthreads();
+  const int pnew = p.k_new ? sh.newpos : -1;
+  if (pnew >= t0 && pnew < t0 + nloc) {  // fused append: the new token's key from the values written
+    if (tid == 0) {
+      if (c.lq4) {  // R16, the arithmetic of append_row_warp: codes replace the values in newlab
+        float a = 0.0f;
+        for (int j = 0; j < r; ++j) a = fmaxf(a, fabsf(sh.newlab[j]));
+        T st = Elem<T>::from_f(a == 0.0f ? 1.0f : a / 7.0f);
+        if (Elem<T>::to_f(st) == 0.0f) st = Elem<T>::from_f(1.0f);
+        const float s = Elem<T>::to_f(st);
+        for (int j = 0; j < r; ++j) sh.newlab[j] = fminf(fmaxf(roundf(sh.newlab[j] / s), -7.0f), 7.0f);
+        sh.newscale = s;
+        if (!perh || hq0 % c.G == 0) {
+          const size_t lr = ((size_t)b * c.Hkv + h) * c.Smax + pnew;
+          uint8_t *cod = (uint8_t *)c.label + lr * c.rb;
+          for (int j = 0; j < r; j += 2) {
+            const int lo = (int)sh.newlab[j], hi = j + 1 < r ? (int)sh.newlab[j + 1] : 0;
+            cod[j >> 1] = (uint8_t)((lo & 15) | ((hi & 15) << 4));
+          }
+          ((T *)c.label_scale)[lr] = st;
+        }
+      }
+      const bool gm = c.greduce == DS_GROUP_MAX;
+      float sc = -INFINITY;
+      for (int g = 0; g < (gm ? G : 1); ++g) {
+        const float *qv = sh.qlab + (gm ? g * r : 0);
+        float acc = 0.0f;
+        for (int j = 0; j < r; ++j) acc = fmaf(qv[j], sh.newlab[j], acc);
+        if (c.lq4) acc = acc * sh.newscale;
+        sc = gm ? fmaxf(sc, acc) : acc;
+      }
+      const int i = pnew - t0;
+      const uint32_t stale = keys[i], fresh = order_key(sc);
+      if (fresh != stale) {
+        atomicSub(&sh.h1[stale >> kSh1], 1u);
+        atomicAdd(&sh.h1[fresh >> kSh1], 1u);
+        keys[i] = fresh;
+      }
+    }
+    __syncthreads();
+  }
   DS_TRACE_AT(1, 1);
 
   // ---- a3 level 1: boundary digit D1 of the cluster histogram

@@ -53,6 +53,10 @@ struct FusedParams {
   float scale_log2;  // log2(e) / sqrt(D)
   int chunk;         // tokens per CTA (cluster of ceil(S / chunk) CTAs per unit)
   int select_only;   // a6 prefetch: lines 1-3 only (idx written, no attention, out unused)
+  // fused a0 (ds_decode_attention_append): one new token per sequence at
+  // positions[b], k_new / v_new [B][1][Hkv][D]; nullptr = no append
+  const void *k_new, *v_new;
+  const int32_t *positions;
 };
 constexpr int kFusedMaxSmem = 227 * 1024;
 bool fused_applicable(const ds_cache *c);
