@@ -113,10 +113,13 @@ __device__ __forceinline__ uint32_t swz(int row, int ch) { return (uint32_t)((ch
 // unit: mbarrier xb of every CTA expects one arrival per CTA.
 __device__ __forceinline__ void xchg_arrive(uint64_t *xb, int nch) {
   const uint32_t a = smem_u32(xb);
+  // one cluster-scope release (cumulative over the CTA's writes ordered
+  // before it by the preceding barrier), then relaxed arrivals
+  asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
   for (int cr = 0; cr < nch; ++cr) {
     uint32_t ra;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(a), "r"(cr));
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(ra) : "memory");
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(ra) : "memory");
   }
 }
 __device__ __forceinline__ void xchg_wait(uint64_t *xb) {
@@ -129,6 +132,36 @@ __device__ __forceinline__ void xchg_wait(uint64_t *xb) {
         : "=r"(done)
         : "r"(a)
         : "memory");
+}
+
+// Cluster barrier without a release per thread (barrier.cluster.arrive
+// defaults to .release, which costs every arriving thread a cluster-scope
+// fence): one fence.acq_rel.cluster per warp by lane 0 -- cumulative over the
+// warp's writes, ordered before it by __syncwarp -- then relaxed arrivals and
+// the acquiring wait.  publish = false: the warp has nothing to release.
+__device__ __forceinline__ void cluster_sync_warp(bool publish) {
+  __syncwarp();
+  if (publish && (threadIdx.x & 31) == 0) asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
+  __syncwarp();
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+}
+
+// cluster_sum of uint2 loads (both halves summed; one 8-B DSMEM load per CTA)
+template <typename F>
+__device__ __forceinline__ uint2 cluster_sum2(int nch, F &&load) {
+  uint2 s = make_uint2(0u, 0u);
+  for (int c0 = 0; c0 < nch; c0 += 8) {
+    uint2 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = c0 + j < nch ? load(c0 + j) : make_uint2(0u, 0u);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      s.x += v[j].x;
+      s.y += v[j].y;
+    }
+  }
+  return s;
 }
 
 // sum over the cluster's CTAs of load(cr): the DSMEM loads of up to 8 CTAs
@@ -511,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     for (int o = 1; o < 16; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if ((tid & 15) == 0) sh.c1[tid >> 4] = v;
   }
-  if constexpr (CL) cluster.sync();
+  if constexpr (CL) cluster_sync_warp(true);
   const int ngrp = (nloc + 31) >> 5;
   uint32_t D1 = 0, need1 = 0;
   bool whole1 = true, ovf = false;
@@ -528,12 +561,14 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       // lane l: bins 63-2l, 62-2l of the (coarse, then fine) histogram, as one u64
       const uint2 *c1p = reinterpret_cast<const uint2 *>(sh.c1) + 31 - lane;
       uint32_t v[2];
-      v[0] = cluster_sum(nch, [&](int cr) { return remote(c1p, cr)->y; });
-      v[1] = cluster_sum(nch, [&](int cr) { return remote(c1p, cr)->x; });
+      uint2 w = cluster_sum2(nch, [&](int cr) { return *remote(c1p, cr); });  // one round trip per 8 CTAs
+      v[0] = w.y;
+      v[1] = w.x;
       const Boundary<2> cb = warp_boundary<2>(v, 63, 0u, (uint32_t)keff);
       const uint2 *h1p = reinterpret_cast<const uint2 *>(sh.h1 + cb.bin * 64) + 31 - lane;
-      v[0] = cluster_sum(nch, [&](int cr) { return remote(h1p, cr)->y; });
-      v[1] = cluster_sum(nch, [&](int cr) { return remote(h1p, cr)->x; });
+      w = cluster_sum2(nch, [&](int cr) { return *remote(h1p, cr); });
+      v[0] = w.y;
+      v[1] = w.x;
       const Boundary<2> fb = warp_boundary<2>(v, cb.bin * 64 + 63, cb.above, (uint32_t)keff);
       if (lane == 0) {
         sh.state[0] = (uint32_t)fb.bin;
@@ -645,10 +680,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     // cluster exchange point x: publish this CTA's data, wait for every CTA's
     auto exchange = [&](int x) {
       sel_sync();
+      DS_TRACE_BY(0, 2 * x, kAttThreads);  // (trace build: the fused kernel borrows kind 0's slots)
       if constexpr (CL) {
         if (stid == 0) xchg_arrive(&sh.xbar[x], nch);
         xchg_wait(&sh.xbar[x]);
       }
+      DS_TRACE_BY(0, 2 * x + 1, kAttThreads);
     };
     // boundary of a cluster 1024-bin histogram (32 coarse sums of 32 per CTA)
     auto boundary1024 = [&](uint32_t *hh, uint32_t *cc, uint32_t need, uint32_t *st, int x) {
@@ -863,8 +900,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         for (int i = keff + stid; i < p.k; i += kSelThreads) idx[i] = -1;
     }
     if constexpr (CL) {  // the attention warps merge the cluster's partials
-      cluster.sync();
-      cluster.sync();
+      cluster_sync_warp(false);
+      cluster_sync_warp(false);
     }
   } else {
     // ================================================== attention warps
@@ -874,8 +911,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     if (p.select_only) {  // a6 prefetch: the selection warps write the index list
       if (ovf) named_sync(kBarDone, kThreads);  // (matches their arrive)
       if constexpr (CL) {
-        cluster.sync();
-        cluster.sync();
+        cluster_sync_warp(false);
+        cluster_sync_warp(false);
       }
       return;
     }
@@ -1177,7 +1214,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     }
     // ---- the cluster's partials -> y (CTA cr finishes a slice of the G*D outputs)
     if constexpr (CL) {
-      cluster.sync();  // every CTA's partial is complete
+      cluster_sync_warp(true);  // every CTA's partial is complete
       const float *cm0 = reinterpret_cast<const float *>(region + GE::PART);
       const int per_cta = (G * D + nch - 1) / nch;
       const int i0 = crank * per_cta, i1 = min(i0 + per_cta, G * D);
@@ -1215,7 +1252,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         }
         outp[i] = Elem<T>::from_f(O / L);
       }
-      cluster.sync();  // partials and exchange data stay alive until every reader is done
+      cluster_sync_warp(true);  // partials and exchange data stay alive until every reader is done
     }
   }
   DS_TRACE_AT(1, 6);
