@@ -638,6 +638,7 @@ def main():
     if not torch.cuda.is_available():
         raise SystemExit("bench.py (ours) needs a CUDA device; there is no CPU fallback")
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    torch.cuda.set_device(dist.local)  # before the NCCL communicator is created
     dist.init("nccl")
     res = run_offload(args, dist) if args.offload else run_ours(args, dist)
     if dist.rank == 0:
