@@ -31,6 +31,14 @@
 // Softmax and the output do not depend on the order in which the selected
 // rows are visited (up to fp32 rounding), which is what lets the attention
 // start before the boundary is resolved.
+//
+// Variants (runtime-uniform branches; everything after the order keys is
+// shared): the label format (16-bit bit copy R8, 4-bit codes + scale R16, or
+// none -- channels read from the K rows, the Table 4 ablation); the GQA
+// reading (group sum R3, max / per query head R17); a fused a0 of the new
+// token (ds_decode_attention_append); select-only for the offload prefetch
+// (a6).  Few units or S > 32K: a thread-block cluster of CTAs per unit, the
+// selection exchanging histograms and members over DSMEM.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <math.h>
@@ -71,6 +79,7 @@ constexpr int kBarAtt = 1, kBarSel = 2, kBarDone = 3, kBarRegs = 4;  // named ba
 // register split after the common phases (64 per thread at launch):
 // attention warpgroups 0-3 grow, selection warpgroups 4-7 shrink
 constexpr int kAttRegs = 88, kSelRegs = 40, kCommonRegs = 64;
+static_assert(kThreads * kCommonRegs <= 65536, "launch register budget (__launch_bounds__(kThreads, 1))");
 static_assert(kAttThreads * kAttRegs + kSelThreads * kSelRegs <= 65536, "register file");
 
 struct alignas(128) Sh {
