@@ -355,3 +355,26 @@ def prefill(cache: LayerCache, K, V, seq_lens, stream=None):
     pos = torch.zeros(B, dtype=torch.int32, device=K.device)
     ds_append_kv(cache, kn, vn, pos, stream=stream)
     cache.seq_lens.copy_(torch.as_tensor(seq_lens, dtype=torch.int32))
+
+
+class CapturedStep:
+    """A decode step built from the calls above (and torch copies), captured
+    once in a CUDA graph on `stream` and replayed: one graph launch per step
+    instead of a Python/ctypes call per kernel and copy.  The graph re-reads
+    the same device and pinned host buffers on every replay, so a caller
+    refreshes their contents between replays.  (Plumbing: the kernels are the
+    ones the captured calls enqueue.)"""
+
+    def __init__(self, fn, stream=None, warmup: int = 1):
+        self.stream = stream if stream is not None else torch.cuda.Stream()
+        with torch.cuda.stream(self.stream):
+            for _ in range(warmup):
+                fn()
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            fn()
+
+    def replay(self):
+        with torch.cuda.stream(self.stream):
+            self.graph.replay()
