@@ -229,6 +229,16 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   const T *lab = (const T *)c.label + lrow * (size_t)c.r;
   const uint8_t *cod = (const uint8_t *)c.label + lrow * (size_t)c.rb;  // 4-bit label (R16)
   const T *scl = (const T *)c.label_scale + lrow;
+  // the query tile goes first, straight into shared memory (cp.async; rows
+  // >= G zero-filled), ahead of the label prefetch in the memory queues; it
+  // is waited for before the prologue's first barrier
+  const T *qb = (const T *)p.q + ((size_t)b * c.Hq + (size_t)hq0) * D;
+  for (int i = tid; i < 8 * CHN; i += kThreads) {
+    const int row = i / CHN, ch = i - (i / CHN) * CHN;
+    cp_async16(smem_u32(sh.qt + row * ROWB + swz(row, ch)), qb + (size_t)min(row, G - 1) * D + ch * 8,
+               row < G ? 16 : 0);
+  }
+  cp_async_commit();
   // fused append: the CTA whose chunk holds the new token writes its K/V
   // rows and (16-bit) label row here and keeps its r channel values; after
   // the stream one thread re-scores it (the stream may have read the old
@@ -294,6 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   T *outp = (T *)p.out + ((size_t)b * c.Hq + (size_t)hq0) * D;
   int32_t *idx = p.idx ? p.idx + (size_t)unit * p.k : nullptr;
   if (n <= 0) {  // empty sequence: y = 0, nothing selected (uniform over the cluster)
+    cp_async_wait<0>();
     if (crank == 0) {
       if (!p.select_only)
         for (int i = tid; i < G * D; i += kThreads) outp[i] = Elem<T>::from_f(0.f);
@@ -305,15 +316,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
 
   // ---- a1, query tile, zeroing (the tile and C are loaded together; q_lab
   // is then summed from the tile in shared memory)
-  const T *qb = (const T *)p.q + ((size_t)b * c.Hq + (size_t)hq0) * D;
   const int r = R > 0 ? R : c.r;
   int chj = 0;
   if (tid < r) chj = c.C[(size_t)h * c.r + tid];
-  for (int i = tid; i < 8 * CHN; i += kThreads) {
-    const int row = i / CHN, ch = i - (i / CHN) * CHN;
-    const uint4 v = row < G ? reinterpret_cast<const uint4 *>(qb + (size_t)row * D)[ch] : make_uint4(0, 0, 0, 0);
-    *reinterpret_cast<uint4 *>(sh.qt + row * ROWB + swz(row, ch)) = v;
-  }
   for (int i = tid; i < kD1; i += kThreads) sh.h1[i] = 0;
   for (int i = tid; i < kD2; i += kThreads) sh.h2[i] = 0;
   for (int i = tid; i < kMaxS / 32; i += kThreads) sh.selm[i] = 0;
@@ -330,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   const bool btc_ok = c.lnone && npg <= (int)(sizeof(sh.cand) / 4);
   if (btc_ok)
     for (int i = tid; i < npg; i += kThreads) btc[i] = __ldg(c.block_table + (size_t)b * c.maxp + pg0 + i);
+  cp_async_wait<0>();  // this thread's part of the query tile
   __syncthreads();
   auto qtile = [&](int g, int ch) {  // q[g][ch] from the swizzled tile
     return Elem<T>::to_f(*reinterpret_cast<const T *>(sh.qt + g * ROWB + swz(g, ch >> 3) + (ch & 7) * 2));
