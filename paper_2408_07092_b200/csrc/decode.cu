@@ -1200,7 +1200,25 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     DS_TRACE_AT(1, 10);
     float *cm = reinterpret_cast<float *>(region + GE::PART);  // [8] m, [8] l, [8][D] o of this CTA
     float *wsc = cm + 16 + 8 * D;                              // [8][16] per-warp weights
-    if (aw < G) {  // warp g: head g's weights over the 16 warps (lane w, w + 16)
+    if constexpr (!CL) {
+      // one CTA: every output thread folds the 16 warp partials of its head
+      // itself (M, then the weights 2^(m_w - M)), no weights phase and barrier
+      for (int i = tid; i < G * D; i += kAttThreads) {
+        const int g = i / D, dd = i - (i / D) * D;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kAttWarps; ++w) M = fmaxf(M, wm[w * 8 + g]);  // finite: >= 1 row (n >= 1)
+        float L = 0.f, O = 0.f;
+#pragma unroll
+        for (int w = 0; w < kAttWarps; ++w) {
+          const float e = exp2f(wm[w * 8 + g] - M);  // 0 for a warp without rows (m = -inf)
+          L = fmaf(wl[w * 8 + g], e, L);
+          O = fmaf(wo[(size_t)(w * 8 + g) * D + dd], e, O);
+        }
+        outp[i] = Elem<T>::from_f(O / L);
+      }
+    }
+    if (CL && aw < G) {  // warp g: head g's weights over the 16 warps (lane w, w + 16)
       const int g = aw;
       const float m0 = lane < kAttWarps ? wm[lane * 8 + g] : -INFINITY;
       float M = m0;
@@ -1210,25 +1228,24 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       float L = lane < kAttWarps ? wl[lane * 8 + g] * e0 : 0.f;
 #pragma unroll
       for (int o2 = 16; o2 > 0; o2 >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o2);
-      // single CTA: fold 1/L into the weights; cluster: keep (M, L) for the merge
-      if (lane < kAttWarps) wsc[g * kAttWarps + lane] = CL ? e0 : e0 / L;
+      // cluster: unnormalised weights; (M, L) go to the merge
+      if (lane < kAttWarps) wsc[g * kAttWarps + lane] = e0;
       if (lane == 0) {
         cm[g] = M;
         cm[8 + g] = L;
       }
     }
-    named_sync(kBarAtt, kAttThreads);
-    DS_TRACE_AT(1, 11);
-    for (int i = tid; i < G * D; i += kAttThreads) {
-      const int g = i / D, dd = i - (i / D) * D;
-      float O = 0.f;
-#pragma unroll
-      for (int w = 0; w < kAttWarps; ++w) O = fmaf(wo[(size_t)(w * 8 + g) * D + dd], wsc[g * kAttWarps + w], O);
-      if constexpr (!CL) outp[i] = Elem<T>::from_f(O);
-      else cm[16 + i] = O;
-    }
     // ---- the cluster's partials -> y (CTA cr finishes a slice of the G*D outputs)
     if constexpr (CL) {
+      named_sync(kBarAtt, kAttThreads);
+      DS_TRACE_AT(1, 11);
+      for (int i = tid; i < G * D; i += kAttThreads) {
+        const int g = i / D, dd = i - (i / D) * D;
+        float O = 0.f;
+#pragma unroll
+        for (int w = 0; w < kAttWarps; ++w) O = fmaf(wo[(size_t)(w * 8 + g) * D + dd], wsc[g * kAttWarps + w], O);
+        cm[16 + i] = O;
+      }
       cluster_sync_warp(true);  // every CTA's partial is complete
       const float *cm0 = reinterpret_cast<const float *>(region + GE::PART);
       const int per_cta = (G * D + nch - 1) / nch;
