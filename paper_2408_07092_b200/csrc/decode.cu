@@ -613,17 +613,19 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         sh.eqm[g] = 0u;
       }
     } else {
-      const int gcmp = whole1 ? (int)D1 - 1 : (int)D1;
-      const uint32_t ecmp = whole1 ? 0xffffffffu : D1;
+      // digit1 > D1 (>= D1 taken whole) <=> key >= gthr; digit1 == D1 <=>
+      // key - (D1 << 20) < 2^20 (never, when D1 is taken whole)
+      const uint32_t gthr = (whole1 ? D1 : D1 + 1) << kSh1;  // (wraps to 0 for D1 = 4095, not whole:)
+      const bool gnone = !whole1 && D1 == (uint32_t)(kD1 - 1);  // nothing lies above the top digit
+      const uint32_t elo = D1 << kSh1, ewid = whole1 ? 0u : (1u << kSh1);
       for (int base = w0; base < w1; base += 128) {
         uint32_t kk[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) kk[e] = keys[base + 32 * e + lane];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const uint32_t d = kk[e] >> kSh1;
-          const uint32_t mg = __ballot_sync(0xffffffffu, (int)d > gcmp);
-          const uint32_t me = __ballot_sync(0xffffffffu, d == ecmp);
+          const uint32_t mg = __ballot_sync(0xffffffffu, !gnone && kk[e] >= gthr);
+          const uint32_t me = __ballot_sync(0xffffffffu, kk[e] - elo < ewid);
           if (lane == e) {
             sh.gtm[(base >> 5) + e] = mg;
             sh.eqm[(base >> 5) + e] = me;
