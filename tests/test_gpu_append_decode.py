@@ -27,6 +27,9 @@ CASES = [
     ("per_head_int4", synth.Config("ad7", B=4, Hq=16, Hkv=4, d=128, S=2500, r=8, k=150, dtype="bf16"), "int4",
      "per_head"),
     ("c1_fp32_two_kernel", synth.CONFIGS["c1"], "native", "sum"),
+    # the bench's launch configuration: c3 at full size, 16-bit and 4-bit label
+    ("c3_full", synth.CONFIGS["c3"], "native", "sum"),
+    ("c3_full_int4", synth.CONFIGS["c3"], "int4", "sum"),
 ]
 
 
@@ -69,6 +72,8 @@ def test_fused_append_equals_append_then_decode(name, cfg, label, group):
         assert torch.equal(a.label, f.label)
     if label == "int4":
         assert torch.equal(a.label_scale.view(torch.int16), f.label_scale.view(torch.int16))
+    del a
+    torch.cuda.empty_cache()
     # the new token is really there: its K row in the pool is k_new
     b = 0
     pg = int(lay.block_table[b, lens[b] // cfg.page_size])
