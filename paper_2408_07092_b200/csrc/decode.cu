@@ -723,7 +723,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
           st[2] = fb.cnt;
         }
       }
+      DS_TRACE_BY(0, 8 + x, kAttThreads);
       sel_sync();
+      DS_TRACE_BY(0, 11 + x, kAttThreads);
     };
     if (tail) {
       boundary1024(sh.h2, sh.c2, need1, sh.state + 3, 0);
@@ -738,6 +740,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         if (pfx > P2 || (whole2 && pfx == P2)) mark(t);
         else if (pfx == P2 && fits2) sh.members[atomicAdd(&sh.nmem, 1u)] = make_uint2(key, (uint32_t)t);
       });
+      DS_TRACE_BY(0, 14, kAttThreads);
       if (!whole2 && fits2) {
         exchange(1);  // every CTA's members are listed
         // the cluster's members land in h2 (no CTA reads it after exchange 1)

@@ -72,7 +72,8 @@ def report(kind, names):
 
 
 if (buf[1][:, 0] > 0).any():  # fused kernel: kind 0 holds its exchange timestamps
-    report_slots(0, [(0, 1, "xchg0 wait"), (1, 2, "level2->xchg1"), (2, 3, "xchg1 wait"), (6, 7, "xchg3 wait")])
+    report_slots(0, [(0, 1, "xchg0 wait"), (1, 8, "L2 dsmem+bnd"), (8, 11, "L2 selsync"), (11, 14, "cand mark"),
+                     (14, 2, "mark->xchg1"), (1, 2, "level2->xchg1"), (2, 3, "xchg1 wait"), (6, 7, "xchg3 wait")])
     report_slots(1, [(2, 0, "masks->xchg0")]) if False else None
 report(0, ["start", "streamed", "S1 D1", "L2 pass", "members", "written", "published"])
 report_slots(0, [(4, 7, "S3 sync"), (7, 8, "gather+rank"), (8, 10, "pre-write"), (10, 5, "write pass")])
