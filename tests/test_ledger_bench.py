@@ -29,6 +29,17 @@ def test_c3_layer_bytes_and_ceiling():
     assert abs(ledger.byte_ratio_ceiling(c3) - 10.6667) < 1e-3
 
 
+def test_int4_label_bytes():
+    """4-bit label (reading R16): ceil(r/2) code bytes + one e-byte scale per
+    token, the layout ds.h documents and LayerCache allocates."""
+    c3 = synth.CONFIGS["c3"]
+    assert ledger.label_row_bytes(8, 2, "int4") == 4 + 2
+    assert ledger.label_row_bytes(3, 2, "int4") == 2 + 2
+    assert ledger.label_row_bytes(16, 4, "int4") == 8 + 4
+    assert ledger.layer_bytes_alg(c3, "int4") == 128 * (32768 * 6 + 2 * 2048 * 128 * 2) == 152 * 2 ** 20
+    assert abs(ledger.byte_ratio_ceiling(c3, "int4") - 2048 / 152) < 1e-9
+
+
 def test_shard_plan_allgather_and_weak():
     sys.path.insert(0, ROOT)
     import bench
