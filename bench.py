@@ -75,6 +75,25 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def read_peak_gbs(dev, gib: float = 4.0, reps: int = 5) -> float:
+    """Read-only streaming bandwidth on this box (context for the roofline:
+    the decode kernel mostly reads, and a copy peak counts writes too):
+    best of `reps` reductions of a `gib` GiB bf16 buffer, CUDA events."""
+    n = int(gib * 2 ** 30) // 2
+    x = torch.ones(n, dtype=torch.bfloat16, device=dev)
+    best = float("inf")
+    for _ in range(reps + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        x.sum(dtype=torch.float32)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del x
+    torch.cuda.empty_cache()
+    return n * 2 / (best / 1e3) / 1e9
+
+
 # ------------------------------------------------------------- dist plumbing
 class Dist:
     def __init__(self):
@@ -339,6 +358,9 @@ def run_ours(args, dist):
                        "algorithmic_bytes_per_launch": bytes_layer}
     # per layer: 1 fused launch on the single-kernel path, else append + 2 decode kernels
     res["gpu_launches"] = args.steps * L * (1 if n_dec == 1 else KERNELS_PER_APPEND + n_dec)
+    rp = read_peak_gbs(dev)
+    res["roofline"]["read_peak_gbs"] = round(rp, 1)  # torch bf16 sum over 4 GiB, context only
+    res["roofline"]["frac_of_read_peak"] = round(achieved / rp, 4)
     if clocks:
         res["clocks"] = clocks
 
