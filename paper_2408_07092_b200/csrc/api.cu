@@ -177,6 +177,8 @@ ds_status ds_decode_attention(const ds_cache *c, const void *q, int32_t k, void 
     fp.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c->head_dim));
     return cuda_status(launch_fused(c, fp, stream));
   }
+  // the two-kernel path has no per-query-head units (R17 per head)
+  if (c->group_reduce == DS_GROUP_PER_HEAD) return DS_ERR_UNSUPPORTED;
   SelectGeom sg = select_geom(c);
   AttnGeom ag = attn_geom(c, k);
   if (ag.nsplit < 1) return DS_ERR_UNSUPPORTED;
@@ -207,6 +209,7 @@ ds_status ds_decode_attention_append(const ds_cache *c, const void *k_new, const
   Workspace w = carve_workspace(c, k, workspace);
   if (!workspace || workspace_bytes < w.bytes || !aligned16(workspace)) return DS_ERR_WORKSPACE_TOO_SMALL;
   if (!fused_applicable(c)) {  // fp32: the append kernel, then the two-kernel decode
+    if (c->group_reduce == DS_GROUP_PER_HEAD) return DS_ERR_UNSUPPORTED;
     if (launch_append(c, k_new, v_new, positions, 1, stream) != cudaSuccess) return DS_ERR_CUDA;
     return ds_decode_attention(c, q, k, out, topk_idx_out, workspace, workspace_bytes, stream);
   }

@@ -667,14 +667,14 @@ struct AttnImpl<float, D, G> {
 
 template <typename T, int D, int G>
 static cudaError_t set_attn_attrs() {
-  static const cudaError_t attr = [] {
+  static PerDeviceOnce once;
+  return once([] {
     cudaError_t e = cudaFuncSetAttribute(AttnImpl<T, D, G>::kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          AttnImpl<T, D, G>::kSmem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(AttnImpl<T, D, G>::kernel(), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return e;
-  }();
-  return attr;
+  });
 }
 
 template <typename T, int D, int G>

@@ -251,7 +251,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       const T *kr = (const T *)p.k_new + ((size_t)b * c.Hkv + h) * D;
       const T *vr = (const T *)p.v_new + ((size_t)b * c.Hkv + h) * D;
       const int32_t *Ch = c.C + (size_t)h * c.r;
-      if (!perh || hq0 % c.G == 0) {
+      // per-head mode: the G units of a KV head all write the identical
+      // bytes (a benign race), so each CTA's own attention gathers read the
+      // new rows after its own writes (ordered by the CTA barriers below)
+      {
         const int page = c.block_table[(size_t)b * c.maxp + pn / c.P];
         const size_t dst = (((size_t)page * c.Hkv + h) * c.P + (pn % c.P)) * (size_t)D;
         for (int v = lane; v < 2 * CHN; v += 32) {
@@ -517,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         const float s = Elem<T>::to_f(st);
         for (int j = 0; j < r; ++j) sh.newlab[j] = fminf(fmaxf(roundf(sh.newlab[j] / s), -7.0f), 7.0f);
         sh.newscale = s;
-        if (!perh || hq0 % c.G == 0) {
+        {  // (per-head mode: every unit of the KV head writes the same bytes)
           const size_t lr = ((size_t)b * c.Hkv + h) * c.Smax + pnew;
           uint8_t *cod = (uint8_t *)c.label + lr * c.rb;
           for (int j = 0; j < r; j += 2) {
@@ -1306,13 +1309,14 @@ static size_t smem_bytes(int chunk) {
 template <typename T, int R, int D, bool CL>
 static cudaError_t launch_cl(const ds_cache *c, const FusedParams &p, int nch, cudaStream_t st) {
   const size_t smem = smem_bytes<T, R, D>(p.chunk);
-  static const cudaError_t attr = [] {
+  static PerDeviceOnce once;
+  const cudaError_t attr = once([] {
     cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, R, D, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kFusedMaxSmem);
     if (e == cudaSuccess && CL)
       e = cudaFuncSetAttribute(decode_kernel<T, R, D, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return e;
-  }();
+  });
   if (attr != cudaSuccess) return attr;
   if (smem > (size_t)kFusedMaxSmem) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
@@ -1335,6 +1339,40 @@ static cudaError_t launch_cl(const ds_cache *c, const FusedParams &p, int nch, c
 template <typename T, int R, int D>
 static cudaError_t launch_t(const ds_cache *c, const FusedParams &p, int nch, cudaStream_t st) {
   return nch > 1 ? launch_cl<T, R, D, true>(c, p, nch, st) : launch_cl<T, R, D, false>(c, p, nch, st);
+}
+
+// Can a cluster of nch CTAs (1024 threads, ~200 KB of shared memory each) be
+// resident at all?  Portable sizes (<= 8) always can on B200; 9..16 need the
+// non-portable opt-in and enough free SMs in one GPC, so ask the occupancy API.
+template <typename T, int R, int D>
+static bool cluster_fits_t(int nch, int chunk) {
+  if (nch <= 8) return true;
+  static PerDeviceOnce once;
+  if (once([] {
+        cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, R, D, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedMaxSmem);
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(decode_kernel<T, R, D, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        return e;
+      }) != cudaSuccess)
+    return false;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nch, 1);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem_bytes<T, R, D>(chunk);
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = nch;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, decode_kernel<T, R, D, true>, &cfg) != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky-free error of the query
+    return false;
+  }
+  return nclusters > 0;
 }
 
 }  // namespace fused
@@ -1364,17 +1402,33 @@ int fused_cluster(const ds_cache *c) {
   return nch;
 }
 
+static int fused_chunk(const ds_cache *c, int nch) {
+  int chunk = (c->max_seq_len + nch - 1) / nch;
+  return (chunk + 127) & ~127;
+}
+
 bool fused_applicable(const ds_cache *c) {
   if (c->dtype != DS_BF16 && c->dtype != DS_FP16) return false;
   if (c->r > fused::kMaxR) return false;
-  return fused_cluster(c) <= 16;
+  const int nch = fused_cluster(c);
+  if (nch > 16) return false;
+  const int chunk = fused_chunk(c, nch);
+  if (chunk > fused::kMaxS) return false;
+  using namespace fused;
+#define DS_F(T)                                                                                                 \
+  if (c->head_dim == 64) return c->r == 8 ? cluster_fits_t<T, 8, 64>(nch, chunk) : cluster_fits_t<T, 0, 64>(nch, chunk); \
+  return c->r == 8 ? cluster_fits_t<T, 8, 128>(nch, chunk) : cluster_fits_t<T, 0, 128>(nch, chunk);
+  if (c->dtype == DS_BF16) {
+    DS_F(__nv_bfloat16)
+  }
+  DS_F(__half)
+#undef DS_F
 }
 
 cudaError_t launch_fused(const ds_cache *c, FusedParams p, cudaStream_t st) {
   using namespace fused;
   const int nch = fused_cluster(c);
-  int chunk = (c->max_seq_len + nch - 1) / nch;
-  chunk = (chunk + 127) & ~127;
+  const int chunk = fused_chunk(c, nch);
   if (chunk > kMaxS) return cudaErrorInvalidValue;
   p.chunk = chunk;
 #define DS_F(T)                                                                                         \

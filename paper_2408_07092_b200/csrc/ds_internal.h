@@ -3,6 +3,8 @@
 #include <cuda_runtime_api.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "ds.h"
 
 namespace ds {
@@ -96,6 +98,27 @@ cudaError_t launch_score(const ds_cache *c, const ScoreParams &p, const SelectGe
 cudaError_t launch_attn(const ds_cache *c, const AttnParams &p, const AttnGeom &g, cudaStream_t st);
 
 CacheView make_view(const ds_cache *c);
+
+// Kernel attributes (dynamic shared memory size, non-portable cluster size)
+// belong to a device context, so a process driving several GPUs must set
+// them once per device, not once per process.  One instance per kernel
+// instantiation; f() is idempotent, so callers racing on a first use may
+// both run it.
+constexpr int kMaxDevices = 64;
+struct PerDeviceOnce {
+  std::atomic<int> done[kMaxDevices] = {};
+  template <typename F>
+  cudaError_t operator()(F &&f) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return f();
+    if (done[dev].load(std::memory_order_acquire)) return cudaSuccess;
+    e = f();
+    if (e == cudaSuccess) done[dev].store(1, std::memory_order_release);
+    return e;
+  }
+};
 
 // cudaLaunchKernelEx with programmatic stream serialization (PDL): the kernel
 // may start while its predecessor drains (see pdl_wait / pdl_trigger).

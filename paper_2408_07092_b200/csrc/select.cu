@@ -573,13 +573,14 @@ __global__ void __launch_bounds__(kThreads, 2) score_select_kernel(ScoreParams p
 // ------------------------------------------------------------- launch
 template <typename T, int R>
 static cudaError_t launch_score_t(const ScoreParams &p, int units, int nch, size_t smem, cudaStream_t st) {
-  static const cudaError_t attr = [] {
+  static PerDeviceOnce once;
+  const cudaError_t attr = once([] {
     cudaError_t e = cudaFuncSetAttribute(score_select_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kMaxDynSmem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(score_select_kernel<T, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return e;
-  }();
+  });
   if (attr != cudaSuccess) return attr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nch, units);

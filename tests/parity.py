@@ -36,9 +36,12 @@ def unit_host(lay, b, h):
     return q, K, V
 
 
-def check_selection(idx_gpu, idx_ref, shat_ref, tau, keff):
+def check_selection(idx_gpu, idx_ref, shat_ref, tau, keff, exact=True):
     """R13: index sets bit-exact except tokens in the symmetric difference
-    whose oracle score lies within 1e-3*max(1,|tau|) of the k-th score."""
+    whose oracle score lies within 1e-3*max(1,|tau|) of the k-th score.
+    exact=True (every label format and GQA reading of this build: line 2 is
+    the oracle's fp32 fma chain in the same order, so s_hat is bit-identical,
+    DESIGN.md R13): the symmetric difference must be empty."""
     g = np.asarray(idx_gpu)
     assert np.all(g[keff:] == -1), "positions >= k_eff must be -1"
     g = g[:keff]
@@ -48,6 +51,8 @@ def check_selection(idx_gpu, idx_ref, shat_ref, tau, keff):
     band = 1e-3 * max(1.0, abs(tau))
     bad = [t for t in sym if abs(float(shat_ref[t]) - tau) > band]
     assert not bad, f"{len(bad)} tokens differ outside the tau band (tau={tau}), e.g. {bad[:5]}"
+    if exact:
+        assert not sym, f"{len(sym)} tokens differ inside the tau band (tau={tau}), e.g. {sorted(sym)[:5]}"
     return len(sym)
 
 
@@ -90,3 +95,47 @@ def check_units(lay, cache, C, k, units, y_gpu, idx_gpu):
             if set(sel.tolist()) == set(idx_ref.tolist()):
                 check_output(y_gpu[b, h * G + g], y_ref[g], cfg.dtype)
     return nsym
+
+
+def check_units_group(lay, cache, group, k, y, idx, units):
+    """check_units for every GQA reading (R3 sum, R17 max / per_head) through
+    oracle.ds_decode_unit_group; idx is [B][Hq][k] for per_head."""
+    cfg = lay.cfg
+    G = cfg.G
+    C = lay.C_plant.numpy()
+    y = y.float().cpu().numpy()
+    idx = idx.cpu().numpy()
+    for b, h in units:
+        q, K, V = unit_host(lay, b, h)
+        S = K.shape[0]
+        if S == 0:
+            continue
+        L = oracle.label_gather(K, C[h])
+        codes = scale = None
+        if cache.label_format == ds.DS_LABEL_INT4:
+            codes, scale = oracle.quantize_label_4bit(L, cfg.dtype)
+        keff = min(k, S)
+        y_ref, i_ref, shat = oracle.ds_decode_unit_group(q, K, V, L, C[h], k, group=group, codes=codes, scale=scale)
+        if group == "per_head":
+            for g in range(G):
+                _, tau = oracle.argtopk(shat[g], k)
+                sel = idx[b, h * G + g]
+                check_selection(sel, i_ref[g][:keff], shat[g], tau, keff)
+                check_output(y[b, h * G + g], oracle.attend(q[g], K, V, sel[:keff]), cfg.dtype)
+                check_output(y[b, h * G + g], y_ref[g], cfg.dtype)
+        else:
+            _, tau = oracle.argtopk(shat, k)
+            sel = idx[b, h]
+            check_selection(sel, i_ref, shat, tau, keff)
+            for g in range(G):
+                check_output(y[b, h * G + g], oracle.attend(q[g], K, V, sel[:keff]), cfg.dtype)
+                check_output(y[b, h * G + g], y_ref[g], cfg.dtype)
+
+
+def sample_units(cfg, n=12, seed=0):
+    """Every unit of a small config; else the first, the last and n-2 seeded ones."""
+    units = [(b, h) for b in range(cfg.B) for h in range(cfg.Hkv)]
+    if len(units) <= n:
+        return units
+    rng = np.random.default_rng(seed)
+    return sorted({units[0], units[-1]} | {units[i] for i in rng.choice(len(units), n - 2, replace=False)})

@@ -4,14 +4,20 @@ ds_append_kv + ds_decode_attention, on identical caches (-m gpu): the same
 index sets bit for bit, the same outputs within R14 (the attention visits
 rows in a run-dependent order), and the same cache contents byte for byte
 afterwards.  The new token differs from what the prefill left at its
-position, so the fused path must not score the stale label row."""
+position, so the fused path must not score the stale label row.
+
+The fused call (the one bench.py times) is also checked against the oracle
+directly: Algorithm 1 on the post-append host K/V -- the
+prefilled tokens plus the new token at its position -- with exact index
+sets (R13) and outputs within R14, for every unit of the small cases and a
+seeded sample of units at c3's full size."""
 import numpy as np
 import pytest
 import torch
 
 import paper_2408_07092_b200 as ds
 import synth
-from parity import check_output
+from parity import check_output, check_units, check_units_group, sample_units
 
 pytestmark = pytest.mark.gpu
 
@@ -78,3 +84,15 @@ def test_fused_append_equals_append_then_decode(name, cfg, label, group):
     b = 0
     pg = int(lay.block_table[b, lens[b] // cfg.page_size])
     assert torch.equal(f.k_pool[pg, :, lens[b] % cfg.page_size], k_new[b, 0])
+    # the fused call against the oracle on the post-append state (Alg. 1):
+    # the host view of every sequence gains the new token at its position
+    bi = torch.arange(cfg.B, device=lay.K.device)
+    pi = pos.long().to(lay.K.device)
+    lay.K[bi, :, pi] = k_new[:, 0]
+    lay.V[bi, :, pi] = v_new[:, 0]
+    lay.seq_lens = (pos + 1).cpu()
+    units = sample_units(cfg, n=12, seed=len(name))
+    if group == "sum":
+        check_units(lay, f, lay.C_plant, cfg.k, units, yf, if_)
+    else:
+        check_units_group(lay, f, group, cfg.k, yf, if_, units)

@@ -11,7 +11,7 @@ import torch
 import oracle
 import paper_2408_07092_b200 as ds
 import synth
-from parity import check_output, check_selection, unit_host
+from parity import check_units_group, unit_host
 
 pytestmark = pytest.mark.gpu
 
@@ -26,34 +26,7 @@ def build(cfg, group, label="native", seq_lens=None, structure="iid"):
 
 
 def check(lay, cache, group, k, y, idx, units):
-    cfg = lay.cfg
-    G = cfg.G
-    C = lay.C_plant.numpy()
-    y = y.float().cpu().numpy()
-    idx = idx.cpu().numpy()
-    for b, h in units:
-        q, K, V = unit_host(lay, b, h)
-        S = K.shape[0]
-        if S == 0:
-            continue
-        L = oracle.label_gather(K, C[h])
-        codes = scale = None
-        if cache.label_format == ds.DS_LABEL_INT4:
-            codes, scale = oracle.quantize_label_4bit(L, cfg.dtype)
-        keff = min(k, S)
-        y_ref, i_ref, shat = oracle.ds_decode_unit_group(q, K, V, L, C[h], k, group=group, codes=codes, scale=scale)
-        if group == "per_head":
-            for g in range(G):
-                _, tau = oracle.argtopk(shat[g], k)
-                sel = idx[b, h * G + g]
-                check_selection(sel, i_ref[g][:keff], shat[g], tau, keff)
-                check_output(y[b, h * G + g], oracle.attend(q[g], K, V, sel[:keff]), cfg.dtype)
-        else:
-            _, tau = oracle.argtopk(shat, k)
-            sel = idx[b, h]
-            check_selection(sel, i_ref, shat, tau, keff)
-            for g in range(G):
-                check_output(y[b, h * G + g], oracle.attend(q[g], K, V, sel[:keff]), cfg.dtype)
+    check_units_group(lay, cache, group, k, y, idx, units)
 
 
 CASES = [

@@ -13,7 +13,7 @@ import torch
 import oracle
 import paper_2408_07092_b200 as ds
 import synth
-from parity import check_output, check_selection, unit_host
+from parity import check_output, check_selection, sample_units, unit_host
 
 pytestmark = pytest.mark.gpu
 
@@ -54,28 +54,33 @@ def test_prefetch_with_true_query_equals_decode():
             assert torch.equal(slot.v_rows[b, h, :ke], lay.V[b, h, t])
 
 
-def test_prefetch_with_predicted_query_matches_oracle():
-    lay, cache = host_cache(CFG, [6000, 5000, 2222, 375])
+C5 = synth.CONFIGS["c5"]
+
+
+@pytest.mark.parametrize("cfg,lens", [(CFG, [6000, 5000, 2222, 375]),
+                                      # c5's full size: S=128K, a cluster of CTAs per unit (select-only)
+                                      (C5, [C5.S, C5.S - 1, 77777, 40000])], ids=["S6000", "c5_full"])
+def test_prefetch_with_predicted_query_matches_oracle(cfg, lens):
+    lay, cache = host_cache(cfg, lens)
     q_hat = synth.predicted_query(lay.q, 0.95, seed=3)
-    slot = ds.ds_prefetch_next_layer(cache, q_hat, CFG.k)
+    slot = ds.ds_prefetch_next_layer(cache, q_hat, cfg.k)
     y = ds.ds_decode_attention_prefetched(cache, lay.q, slot)
     torch.cuda.synchronize()
     C = lay.C_plant.numpy()
-    G = CFG.G
+    G = cfg.G
     jac = []
-    for b in range(CFG.B):
-        for h in range(CFG.Hkv):
-            q, K, V = unit_host(lay, b, h)
-            qh = q_hat[b, h * G:(h + 1) * G].float().cpu().numpy()
-            L = oracle.label_gather(K, C[h])
-            shat = oracle.approx_scores(oracle.query_label(qh, C[h]), L)
-            ref_idx, tau = oracle.argtopk(shat, CFG.k)
-            ke = min(CFG.k, K.shape[0])
-            sel = slot.idx[b, h].cpu().numpy()
-            check_selection(sel, ref_idx, shat, tau, ke)
-            for g in range(G):
-                check_output(y[b, h * G + g].float().cpu().numpy(), oracle.attend(q[g], K, V, sel[:ke]), "bf16")
-            _, true_idx, _, _ = oracle.ds_decode_unit(q, K, V, L, C[h], CFG.k)
-            jac.append(len(set(sel[:ke].tolist()) & set(true_idx.tolist())) / len(set(sel[:ke].tolist()) |
-                                                                                  set(true_idx.tolist())))
+    for b, h in sample_units(cfg, n=12):
+        q, K, V = unit_host(lay, b, h)
+        qh = q_hat[b, h * G:(h + 1) * G].float().cpu().numpy()
+        L = oracle.label_gather(K, C[h])
+        shat = oracle.approx_scores(oracle.query_label(qh, C[h]), L)
+        ref_idx, tau = oracle.argtopk(shat, cfg.k)
+        ke = min(cfg.k, K.shape[0])
+        sel = slot.idx[b, h].cpu().numpy()
+        check_selection(sel, ref_idx, shat, tau, ke)
+        for g in range(G):
+            check_output(y[b, h * G + g].float().cpu().numpy(), oracle.attend(q[g], K, V, sel[:ke]), "bf16")
+        _, true_idx, _, _ = oracle.ds_decode_unit(q, K, V, L, C[h], cfg.k)
+        sa, st = set(sel[:ke].tolist()), set(true_idx.tolist())
+        jac.append(len(sa & st) / len(sa | st))
     assert np.mean(jac) > 0.2  # the predicted query selects overlapping tokens (diagnostic floor)

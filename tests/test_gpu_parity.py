@@ -11,7 +11,7 @@ import torch
 import oracle
 import paper_2408_07092_b200 as ds
 import synth
-from parity import build_cache, check_output, check_units, unit_host
+from parity import build_cache, check_output, check_units, sample_units, unit_host
 
 pytestmark = pytest.mark.gpu
 
@@ -216,15 +216,11 @@ FULL = ["c2_32k", "c3", "c4", "c5"]
 @pytest.mark.parametrize("name", FULL)
 def test_full_size_sampled_units(name):
     """BASELINE.json sizes in the bench launch configuration; the oracle
-    checks a sample of units (first, last and two seeded random ones)."""
+    checks a sample of units (first, last and ten seeded random ones)."""
     cfg = synth.CONFIGS[name]
     lay, cache, C = build_cache(cfg)
     y, idx = run_decode(cache, lay, cfg.k)
-    rng = np.random.default_rng(0)
-    units = {(0, 0), (cfg.B - 1, cfg.Hkv - 1)}
-    while len(units) < 4:
-        units.add((int(rng.integers(cfg.B)), int(rng.integers(cfg.Hkv))))
-    check_units(lay, cache, C, cfg.k, sorted(units), y, idx)
+    check_units(lay, cache, C, cfg.k, sample_units(cfg, n=12), y, idx)
     # properties at every unit: ascending, distinct, in range, exact count
     iv = idx.cpu()
     assert (iv[..., 1:] > iv[..., :-1]).all() and (iv >= 0).all() and (iv < cfg.S).all()
