@@ -94,6 +94,52 @@ def read_peak_gbs(dev, gib: float = 4.0, reps: int = 5) -> float:
     return n * 2 / (best / 1e3) / 1e9
 
 
+# ------------------------------------------------- per-kernel device times
+def kernel_trace(fn, reps: int = 3):
+    """Every kernel that fn() launches (fn run `reps` times, synchronised),
+    with its device duration, as recorded by CUPTI through torch.profiler
+    (kineto) -- CUDA-graph replays included.  Not a profiler replay: the
+    kernels run once, in situ, at their normal clocks; only the activity
+    records are collected.  Returns [{name, ts, dur (us), stream}]."""
+    import tempfile
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+    path = tempfile.mktemp(suffix=".json")
+    prof.export_chrome_trace(path)
+    with open(path) as f:
+        ev = json.load(f).get("traceEvents", [])
+    os.unlink(path)
+    out = [{"name": e["name"], "ts": float(e["ts"]), "dur": float(e["dur"]),
+            "stream": e.get("args", {}).get("stream")} for e in ev if e.get("cat") == "kernel"]
+    return sorted(out, key=lambda e: e["ts"])
+
+
+def summarize_kernels(ks, steps: int):
+    """Per kernel name: launches, mean / median / min / max duration (us), and
+    the share of the device time; plus the summed kernel time per step."""
+    by = {}
+    for k in ks:
+        by.setdefault(k["name"], []).append(k["dur"])
+    tot = sum(k["dur"] for k in ks)
+    rows = {n: {"launches": len(v), "mean_us": round(statistics.mean(v), 3),
+                "median_us": round(statistics.median(v), 3), "min_us": round(min(v), 3),
+                "max_us": round(max(v), 3), "share": round(sum(v) / tot, 4) if tot else None}
+            for n, v in by.items()}
+    return {"kernels": rows, "kernel_us_per_step": round(tot / max(1, steps), 3)}
+
+
+def short_name(n: str) -> str:
+    for key in ("decode_kernel", "attn_mma_kernel", "attn_simt_kernel", "score_select_kernel", "gather_rows_kernel",
+                "append_kernel"):
+        if key in n:
+            return key
+    return n[:80]
+
+
 # ------------------------------------------------------------- dist plumbing
 class Dist:
     def __init__(self):
@@ -305,6 +351,10 @@ def run_ours(args, dist):
             if gathered is not None:
                 shard.allgather_heads(dist.pg, ly["out"], gathered[i])   # the path's one exchange step
 
+    def decode_only_layer(ly):
+        ds._check(lib.ds_decode_attention(ctypes.byref(ly["cs"]), P(ly["q"].data_ptr()), k, P(ly["out"].data_ptr()),
+                                          None, P(ws.data_ptr()), ws.numel(), sp), "decode")
+
     def decode_only():
         for ly in layers:
             ds._check(lib.ds_decode_attention(ctypes.byref(ly["cs"]), P(ly["q"].data_ptr()), k,
@@ -313,13 +363,27 @@ def run_ours(args, dist):
 
     cpath = os.path.join(ROOT, "gpurun_out", f"clocks_rank{dist.rank}.csv")
     os.makedirs(os.path.dirname(cpath), exist_ok=True)
-    ms_total, _, clocks = time_graph(step, args.steps, args.warmup, dist, stream,
-                                     sampler=lambda: Clocks(dist.local, cpath))
+    ms_total, g_step, clocks = time_graph(step, args.steps, args.warmup, dist, stream,
+                                          sampler=lambda: Clocks(dist.local, cpath))
     ms_step = dist.max(ms_total / args.steps)
 
     # dominant launch group for the roofline: ds_decode_attention alone over the same layers
-    ms_dec_total, _ = time_graph(decode_only, args.steps, 2, dist, stream)
+    ms_dec_total, g_dec = time_graph(decode_only, args.steps, 2, dist, stream)
     us_decode = dist.max(ms_dec_total / args.steps) / L * 1000.0
+
+    # in-situ device time of every kernel of the two timed graphs (CUPTI via
+    # torch.profiler, three more replays each), and of one decode launch in
+    # isolation after an L2 flush
+    with torch.cuda.stream(stream):
+        ks_step = kernel_trace(g_step.replay, reps=3)
+        ks_dec = kernel_trace(g_dec.replay, reps=3)
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+        def iso():
+            flush.zero_()                      # 512 MiB written: L2 (126 MB) holds nothing of layer 0
+            decode_only_layer(layers[0])
+        ks_iso = [x for x in kernel_trace(iso, reps=10) if "decode_kernel" in x["name"]]
+        del flush
 
     bytes_layer = ledger.layer_bytes_alg(cfg, args.label)
     n_ranks = dist.world
@@ -359,6 +423,28 @@ def run_ours(args, dist):
                        "algorithmic_bytes_per_launch": bytes_layer}
     # per layer: 1 fused launch on the single-kernel path, else append + 2 decode kernels
     res["gpu_launches"] = args.steps * L * (1 if n_dec == 1 else KERNELS_PER_APPEND + n_dec)
+    # CUPTI in-situ durations: the dominant kernel's share of the step, and
+    # the roofline fraction of its mean in-situ launch and of one isolated launch
+    sd, ss = summarize_kernels(ks_dec, 3), summarize_kernels(ks_step, 3)
+    dom = [n for n in sd["kernels"] if short_name(n) in ("decode_kernel", "score_select_kernel")]
+    if dom:
+        du = sd["kernels"][dom[0]]["mean_us"]
+        res["roofline"]["cupti_us_per_launch"] = du
+        res["roofline"]["cupti_frac"] = round(bytes_layer / (du * 1e-6) / 1e9 / hbm_peak, 4)
+    if ks_iso:
+        iu = statistics.median(x["dur"] for x in ks_iso)
+        res["roofline"]["isolated_us"] = round(iu, 3)
+        res["roofline"]["isolated_frac"] = round(bytes_layer / (iu * 1e-6) / 1e9 / hbm_peak, 4)
+    res["kernel_trace"] = {
+        "source": "CUPTI kernel activity (torch.profiler), 3 extra replays of each timed graph",
+        "step_graph": {short_name(n): v for n, v in ss["kernels"].items()},
+        "step_kernel_us": ss["kernel_us_per_step"], "step_us_events": round(ms_step * 1e3, 3),
+        "decode_graph": {short_name(n): v for n, v in sd["kernels"].items()},
+        "decode_kernel_us": sd["kernel_us_per_step"], "decode_us_events": round(us_decode * L, 3)}
+    tname = f"kernels_{full.name}" + ("_int4" if args.label == "int4" else "") + f"_rank{dist.rank}.json"
+    with open(os.path.join(ROOT, "gpurun_out", tname), "w") as f:
+        json.dump({"summary": res["kernel_trace"], "isolated_decode_us": [x["dur"] for x in ks_iso],
+                   "step_graph_kernels": [{**x, "name": short_name(x["name"])} for x in ks_step]}, f, indent=1)
     rp = read_peak_gbs(dev)
     res["roofline"]["read_peak_gbs"] = round(rp, 1)  # torch bf16 sum over 4 GiB, context only
     res["roofline"]["frac_of_read_peak"] = round(achieved / rp, 4)
