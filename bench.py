@@ -118,16 +118,34 @@ def kernel_trace(fn, reps: int = 3):
     return sorted(out, key=lambda e: e["ts"])
 
 
+def exclusive_times(ks):
+    """Per launch, the device time no earlier launch already covers:
+    end_i - max(start_i, latest end before it).  With programmatic dependent
+    launch a kernel's CTAs start on idle SMs while its predecessor drains and
+    then wait at griddepcontrol.wait, so raw durations overlap and over-count;
+    the exclusive times sum to the union of the kernel intervals (<= the
+    step's event time)."""
+    out, end = [], float("-inf")
+    for k in sorted(ks, key=lambda e: e["ts"]):
+        e = k["ts"] + k["dur"]
+        out.append(max(0.0, e - max(k["ts"], end)))
+        end = max(end, e)
+    return out
+
+
 def summarize_kernels(ks, steps: int):
-    """Per kernel name: launches, mean / median / min / max duration (us), and
-    the share of the device time; plus the summed kernel time per step."""
-    by = {}
-    for k in ks:
+    """Per kernel name: launches, mean / median / min / max raw duration (us),
+    the mean exclusive time (exclusive_times) and its share of the busy time;
+    plus the busy (union) kernel time per step."""
+    by, ex = {}, {}
+    for k, x in zip(sorted(ks, key=lambda e: e["ts"]), exclusive_times(ks)):
         by.setdefault(k["name"], []).append(k["dur"])
-    tot = sum(k["dur"] for k in ks)
+        ex.setdefault(k["name"], []).append(x)
+    tot = sum(sum(v) for v in ex.values())
     rows = {n: {"launches": len(v), "mean_us": round(statistics.mean(v), 3),
                 "median_us": round(statistics.median(v), 3), "min_us": round(min(v), 3),
-                "max_us": round(max(v), 3), "share": round(sum(v) / tot, 4) if tot else None}
+                "max_us": round(max(v), 3), "excl_mean_us": round(statistics.mean(ex[n]), 3),
+                "share": round(sum(ex[n]) / tot, 4) if tot else None}
             for n, v in by.items()}
     return {"kernels": rows, "kernel_us_per_step": round(tot / max(1, steps), 3)}
 
@@ -377,10 +395,12 @@ def run_ours(args, dist):
     with torch.cuda.stream(stream):
         ks_step = kernel_trace(g_step.replay, reps=3)
         ks_dec = kernel_trace(g_dec.replay, reps=3)
-        flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        flush = torch.ones(256 << 20, dtype=torch.bfloat16, device=dev)
 
         def iso():
-            flush.zero_()                      # 512 MiB written: L2 (126 MB) holds nothing of layer 0
+            # 512 MiB READ: L2 (126 MB) holds nothing of layer 0 and no dirty
+            # lines whose write-back the decode would pay for
+            flush.sum(dtype=torch.float32)
             decode_only_layer(layers[0])
         ks_iso = [x for x in kernel_trace(iso, reps=10) if "decode_kernel" in x["name"]]
         del flush
@@ -428,7 +448,7 @@ def run_ours(args, dist):
     sd, ss = summarize_kernels(ks_dec, 3), summarize_kernels(ks_step, 3)
     dom = [n for n in sd["kernels"] if short_name(n) in ("decode_kernel", "score_select_kernel")]
     if dom:
-        du = sd["kernels"][dom[0]]["mean_us"]
+        du = sd["kernels"][dom[0]]["excl_mean_us"]
         res["roofline"]["cupti_us_per_launch"] = du
         res["roofline"]["cupti_frac"] = round(bytes_layer / (du * 1e-6) / 1e9 / hbm_peak, 4)
     if ks_iso:

@@ -75,7 +75,7 @@ constexpr int kCandCap = 2048;        // digit-1 boundary tokens listed
 constexpr int kMaxMembers = 512;      // 22-bit-prefix boundary tokens ranked directly
 constexpr int kListCap = 2048 + 64;   // pool rows per attention round (k = 2048 + batch alignment)
 constexpr int kBatch = 8;             // rows per warp batch
-constexpr int kBarAtt = 1, kBarSel = 2, kBarRegs = 4;  // named barriers
+constexpr int kBarAtt = 1, kBarSel = 2, kBarDone = 3, kBarRegs = 4;  // named barriers
 // register split after the common phases (64 per thread at launch):
 // attention warpgroups 0-3 grow, selection warpgroups 4-7 shrink
 constexpr int kAttRegs = 88, kSelRegs = 40, kCommonRegs = 64;
@@ -96,7 +96,6 @@ struct alignas(128) Sh {
   uint32_t list[kListCap];     // pool row ids of the current attention round
   uint32_t wtot[kWarps];
   uint32_t state[16];
-  uint32_t kfree[16];          // selection warp w no longer reads keys of groups [64 w, 64 w + 64)
   uint32_t cnt[4];             // [3] this CTA's selected count (read remotely)
   uint32_t ncand, nmem, lower_sel, pad0;
   uint64_t xbar[4];            // cluster exchange barriers of the selection warps
@@ -331,11 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     sh.ncand = 0;
     sh.nmem = 0;
     sh.lower_sel = 0;
-    sh.state[10] = 0u;  // gtm and n_gt (state[11]) published by the attention warps
-    sh.state[14] = 0u;  // candidate rows not listed yet (read by the attention warps)
-    sh.state[15] = 0u;  // the attention warps' batch cursor
   }
-  if (tid < 16) sh.kfree[tid] = 0u;
   // DS_LABEL_NONE: the chunk's block-table entries (cand is free until the masks)
   int32_t *btc = reinterpret_cast<int32_t *>(sh.cand);
   const int pg0 = t0 / c.P;
@@ -608,20 +603,66 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   DS_TRACE_AT(1, 7);
   const bool tail = !all_sel && !whole1;
 
-  // Per 32-token group g, two ballot masks over the order keys: gtm = digit1
-  // > D1 (>= D1 when D1 is taken whole: every such token is selected) and
-  // eqm = digit1 == D1 (the boundary candidates).  Right after the role split
-  // below, attention warp w builds gtm for groups [64 w, 64 w + 64) and lists
-  // those rows (its gathers start at once), while selection warp w builds eqm
-  // and the candidate list over the same groups -- the attention warp's ring
-  // stages alias exactly those keys, so it waits only for its partner's flag.
-  // digit1 > D1 (>= D1 taken whole) <=> key >= gthr; digit1 == D1 <=>
-  // key - (D1 << 20) < 2^20 (never, when D1 is taken whole)
-  const uint32_t gthr = (whole1 ? D1 : D1 + 1) << kSh1;  // (wraps to 0 for D1 = 4095, not whole:)
-  const bool gnone = !whole1 && D1 == (uint32_t)(kD1 - 1);  // nothing lies above the top digit
-  const uint32_t elo = D1 << kSh1, ewid = whole1 ? 0u : (1u << kSh1);
-  constexpr int kGrpW = kMaxS / 32 / kAttWarps;  // groups per warp (64)
-  static_assert(kGrpW == 64 && kAttWarps == kSelWarps, "warp w of each role owns groups [64 w, 64 w + 64)");
+  // ---- masks: per 32-token group, ballot of digit1 > D1 (>= D1 when D1 is
+  // taken whole) and digit1 == D1; warp w owns groups of [w*per, w*per+per)
+  {
+    int per = (nloc + kWarps - 1) / kWarps;
+    per = (per + 127) & ~127;
+    const int w0 = min(warp * per, nloc), w1 = min(w0 + per, nloc);
+    if (all_sel) {
+      for (int g = tid; g < ngrp; g += kThreads) {
+        const int rem = nloc - g * 32;
+        sh.gtm[g] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+        sh.eqm[g] = 0u;
+      }
+    } else {
+      // digit1 > D1 (>= D1 taken whole) <=> key >= gthr; digit1 == D1 <=>
+      // key - (D1 << 20) < 2^20 (never, when D1 is taken whole)
+      const uint32_t gthr = (whole1 ? D1 : D1 + 1) << kSh1;  // (wraps to 0 for D1 = 4095, not whole:)
+      const bool gnone = !whole1 && D1 == (uint32_t)(kD1 - 1);  // nothing lies above the top digit
+      const uint32_t elo = D1 << kSh1, ewid = whole1 ? 0u : (1u << kSh1);
+      for (int base = w0; base < w1; base += 128) {
+        uint32_t kk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) kk[e] = keys[base + 32 * e + lane];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t mg = __ballot_sync(0xffffffffu, !gnone && kk[e] >= gthr);
+          const uint32_t me = __ballot_sync(0xffffffffu, kk[e] - elo < ewid);
+          if (lane == e) {
+            sh.gtm[(base >> 5) + e] = mg;
+            sh.eqm[(base >> 5) + e] = me;
+          }
+        }
+      }
+      __syncwarp();
+      DS_TRACE_AT(1, 8);
+      if (!whole1) {  // the D1 tokens: candidate list + digit-2 histogram (lane per group)
+        const int ng = (w1 - w0 + 31) >> 5, grp = (w0 >> 5) + lane;
+        uint32_t e = lane < ng ? sh.eqm[grp] : 0u;
+        const uint32_t ne = __popc(e);
+        uint32_t incl = ne;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        uint32_t slot = 0;
+        if (lane == 31 && incl && !ovf) slot = atomicAdd(&sh.ncand, incl);
+        slot = __shfl_sync(0xffffffffu, slot, 31) + incl - ne;
+        while (e) {
+          const int bit = __ffs(e) - 1;
+          e &= e - 1;
+          const uint32_t key = keys[grp * 32 + bit];
+          atomicAdd(&sh.h2[(key >> kSh2) & (kD2 - 1)], 1u);
+          if (!ovf) sh.cand[slot++] = make_uint2(key, (uint32_t)(t0 + grp * 32 + bit));
+        }
+      }
+    }
+  }
+  DS_TRACE_AT(1, 9);
+  __syncthreads();
+  DS_TRACE_AT(1, 2);
 
   const int32_t *bt = c.block_table + (size_t)b * c.maxp;
   const bool pow2 = (c.P & (c.P - 1)) == 0;
@@ -631,7 +672,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     const int sl = t - pg * c.P;
     return ((uint32_t)__ldg(bt + pg) * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P + (uint32_t)sl;
   };
-  DS_TRACE_AT(1, 2);
+  if (tid == 0) {
+    sh.state[14] = 0u;  // candidate rows not listed yet (read by the attention warps)
+    sh.state[15] = 0u;  // the attention warps' batch cursor
+  }
+  __syncthreads();
 
   if (warp >= kAttWarps) {
     // ================================================ selection tail
@@ -639,58 +684,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     named_sync(kBarRegs, kThreads);  // the attention warps hold their registers
     pdl_trigger();
     const int stid = tid - kAttThreads, sw = warp - kAttWarps;
-    DS_TRACE_BY(1, 14, kAttThreads);
-    // ---- eqm + candidate list (+ digit-2 histogram) over groups [64 sw, 64 sw + 64)
-    auto keys_free = [&] {  // the partner attention warp may now overwrite those keys
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();
-        *reinterpret_cast<volatile uint32_t *>(&sh.kfree[sw]) = 1u;
-      }
-    };
-    if (tail) {
-      const int g0 = sw * kGrpW;
-      uint32_t ea = 0u, eb = 0u;  // lane l: eqm of groups g0 + l and g0 + 32 + l
-#pragma unroll 8  // (40 registers in this role)
-      for (int gi = 0; gi < 32; ++gi) {
-        const int ta_ = (g0 + gi) * 32 + lane, tb_ = ta_ + 32 * 32;
-        const uint32_t ka = keys[ta_], kb = keys[tb_];
-        const uint32_t ma = __ballot_sync(0xffffffffu, ta_ < nloc && ka - elo < ewid);
-        const uint32_t mb = __ballot_sync(0xffffffffu, tb_ < nloc && kb - elo < ewid);
-        ea = lane == gi ? ma : ea;
-        eb = lane == gi ? mb : eb;
-      }
-      sh.eqm[g0 + lane] = ea;
-      sh.eqm[g0 + 32 + lane] = eb;
-      const uint32_t ne = __popc(ea) + __popc(eb);
-      uint32_t incl = ne;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      uint32_t slot = 0;
-      if (lane == 31 && incl && !ovf) slot = atomicAdd(&sh.ncand, incl);
-      slot = __shfl_sync(0xffffffffu, slot, 31) + incl - ne;
-      for (int part = 0; part < 2; ++part) {
-        const int grp = g0 + 32 * part + lane;
-        for (uint32_t e = part ? eb : ea; e; e &= e - 1) {
-          const int bit = __ffs(e) - 1;
-          const uint32_t key = keys[grp * 32 + bit];
-          atomicAdd(&sh.h2[(key >> kSh2) & (kD2 - 1)], 1u);
-          if (!ovf) sh.cand[slot++] = make_uint2(key, (uint32_t)(t0 + grp * 32 + bit));
-        }
-      }
-    }
-    if (!ovf) keys_free();  // (overflow: the tail still scans the keys)
-    named_sync(kBarSel, kSelThreads);  // candidates, ncand and h2 complete
-    DS_TRACE_BY(1, 15, kAttThreads);
-    auto wait_gtm = [&] {  // gtm and n_gt published by the attention warps
-      if (lane == 0)
-        while (*reinterpret_cast<volatile uint32_t *>(&sh.state[10]) == 0u) __nanosleep(32);
-      __syncwarp();
-      __threadfence_block();
-    };
     auto for_each_cand = [&](auto &&f) {  // (key, global token) with digit1 == D1, this CTA
       if (!ovf) {
         const int nc = (int)sh.ncand;
@@ -739,6 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     };
     if (tail) {
       boundary1024(sh.h2, sh.c2, need1, sh.state + 3, 0);
+      DS_TRACE_BY(1, 14, kAttThreads);
       const uint32_t P2 = (D1 << (kSh1 - kSh2)) | sh.state[3];
       const uint32_t need2 = need1 - sh.state[4];
       const uint32_t cnt2 = sh.state[5];
@@ -775,6 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
           gathered[i] = remote(sh.members, cr)[i - (int)sh.c2[cr]];
         }
         sel_sync();
+        DS_TRACE_BY(1, 15, kAttThreads);
         const int nm = (int)cnt2;  // rank by (key desc, token asc)
         for (int i = stid; i < nm; i += kSelThreads) {
           const uint2 me = gathered[i];
@@ -842,7 +837,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       sel_sync();  // every mark is in selm
     }
     if (ovf) {
-      keys_free();  // the attention warps wait for the keys buffer
+      named_arrive(kBarDone, kThreads);  // the attention warps wait for the keys buffer
     } else {
       // the selected candidates' row ids go to list positions [n_gt, n_gt + n_sel),
       // behind the attention warps' own list of the certain rows; then a flag
@@ -850,6 +845,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       const int ga = sw * 64 + lane, gb = ga + 32;  // warp sw: groups [64 sw, 64 sw + 64)
       const uint32_t ma = (tail && ga < ngrp) ? sh.selm[ga] : 0u;
       const uint32_t mb = (tail && gb < ngrp) ? sh.selm[gb] : 0u;
+      uint32_t gt = (ga < ngrp ? __popc(sh.gtm[ga]) : 0u) + (gb < ngrp ? __popc(sh.gtm[gb]) : 0u);
       const uint32_t ca = __popc(ma), cb = __popc(mb);
       uint32_t ia = ca, ib = cb;
 #pragma unroll
@@ -861,17 +857,21 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
           ib += yb;
         }
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gt += __shfl_xor_sync(0xffffffffu, gt, o);
       const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31), tb = __shfl_sync(0xffffffffu, ib, 31);
-      if (lane == 0) sh.wtot[kAttWarps + sw] = ta + tb;
+      if (lane == 0) {
+        sh.wtot[kAttWarps + sw] = ta + tb;
+        sh.cand[sw].x = gt;  // (the candidate list is no longer read)
+      }
       sel_sync();
-      uint32_t base = 0, n_sel = 0;
+      uint32_t base = 0, n_sel = 0, n_gt = 0;
       for (int w = 0; w < kSelWarps; ++w) {
         const uint32_t x = sh.wtot[kAttWarps + w];
         if (w < sw) base += x;
         n_sel += x;
+        n_gt += sh.cand[w].x;
       }
-      wait_gtm();
-      const uint32_t n_gt = sh.state[11];
       const uint32_t p0 = (n_gt + kBatch - 1) & ~(uint32_t)(kBatch - 1);  // batch-aligned start
       const bool fits = p0 + n_sel <= (uint32_t)kListCap;
       if (fits) {
@@ -890,7 +890,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     DS_TRACE_BY(1, 3, kAttThreads);
     // ---- optional index list: ascending selected tokens, -1 past k_eff
     if (idx) {
-      wait_gtm();
       const int ga = sw * 64 + lane, gb = ga + 32;  // warp sw: groups [64 sw, 64 sw + 64)
       const uint32_t ma = ga < ngrp ? (sh.gtm[ga] | sh.selm[ga]) : 0u;
       const uint32_t mb = gb < ngrp ? (sh.gtm[gb] | sh.selm[gb]) : 0u;
@@ -932,63 +931,15 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kAttRegs));
     named_arrive(kBarRegs, kThreads);
     pdl_trigger();
-    const int aw = warp;
-    // ---- gtm over groups [64 aw, 64 aw + 64): lane l holds groups ga = 64 aw + l, gb = ga + 32
-    const int ga = aw * kGrpW + lane, gb = ga + 32;
-    uint32_t ma = 0u, mb = 0u;
-    {
-      const int g0 = aw * kGrpW;
-#pragma unroll
-      for (int gi = 0; gi < 32; ++gi) {
-        const int ta_ = (g0 + gi) * 32 + lane, tb_ = ta_ + 32 * 32;
-        const uint32_t ka = keys[ta_], kb = keys[tb_];
-        const uint32_t xa = __ballot_sync(0xffffffffu, ta_ < nloc && (all_sel || (!gnone && ka >= gthr)));
-        const uint32_t xb = __ballot_sync(0xffffffffu, tb_ < nloc && (all_sel || (!gnone && kb >= gthr)));
-        ma = lane == gi ? xa : ma;
-        mb = lane == gi ? xb : mb;
-      }
-    }
-    sh.gtm[ga] = ma;
-    sh.gtm[gb] = mb;
-    const uint32_t ca = __popc(ma), cb = __popc(mb);
-    uint32_t ia = ca, ib = cb;
-#pragma unroll
-    for (int o2 = 1; o2 < 32; o2 <<= 1) {
-      const uint32_t ya = __shfl_up_sync(0xffffffffu, ia, o2);
-      const uint32_t yb = __shfl_up_sync(0xffffffffu, ib, o2);
-      if (lane >= o2) {
-        ia += ya;
-        ib += yb;
-      }
-    }
-    const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31), tb = __shfl_sync(0xffffffffu, ib, 31);
-    if (lane == 0) sh.wtot[aw] = ta + tb;
-    named_sync(kBarAtt, kAttThreads);  // every gtm word and warp total written
-    uint32_t gbase = 0, n_gt = 0;
-    for (int w = 0; w < kAttWarps; ++w) {
-      const uint32_t x = sh.wtot[w];
-      if (w < aw) gbase += x;
-      n_gt += x;
-    }
-    if (tid == 0) {  // publish gtm and n_gt to the selection warps
-      sh.state[11] = n_gt;
-      __threadfence_block();
-      *reinterpret_cast<volatile uint32_t *>(&sh.state[10]) = 1u;
-    }
-    DS_TRACE_AT(1, 8);
     if (p.select_only) {  // a6 prefetch: the selection warps write the index list
+      if (ovf) named_sync(kBarDone, kThreads);  // (matches their arrive)
       if constexpr (CL) {
         cluster_sync_warp(false);
         cluster_sync_warp(false);
       }
       return;
     }
-    auto wait_keys_free = [&] {  // the partner selection warp no longer reads this warp's ring keys
-      if (lane == 0)
-        while (*reinterpret_cast<volatile uint32_t *>(&sh.kfree[aw]) == 0u) __nanosleep(32);
-      __syncwarp();
-      __threadfence_block();
-    };
+    const int aw = warp;
     const int gq = lane >> 2, tq = lane & 3;
     const uint8_t *kp = (const uint8_t *)c.k_pool;
     const uint8_t *vp = (const uint8_t *)c.v_pool;
@@ -1133,12 +1084,34 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
 
     if (!ovf) {
       // the certain rows (digit1 > D1) at list positions [0, n_gt)
+      const int ga = aw * 64 + lane, gb = ga + 32;  // warp aw: groups [64 aw, 64 aw + 64)
+      const uint32_t ma = ga < ngrp ? sh.gtm[ga] : 0u;
+      const uint32_t mb = gb < ngrp ? sh.gtm[gb] : 0u;
+      const uint32_t ca = __popc(ma), cb = __popc(mb);
+      uint32_t ia = ca, ib = cb;
+#pragma unroll
+      for (int o2 = 1; o2 < 32; o2 <<= 1) {
+        const uint32_t ya = __shfl_up_sync(0xffffffffu, ia, o2);
+        const uint32_t yb = __shfl_up_sync(0xffffffffu, ib, o2);
+        if (lane >= o2) {
+          ia += ya;
+          ib += yb;
+        }
+      }
+      const uint32_t ta = __shfl_sync(0xffffffffu, ia, 31), tb = __shfl_sync(0xffffffffu, ib, 31);
+      if (lane == 0) sh.wtot[aw] = ta + tb;
+      named_sync(kBarAtt, kAttThreads);
+      uint32_t base = 0, n_gt = 0;
+      for (int w = 0; w < kAttWarps; ++w) {
+        const uint32_t x = sh.wtot[w];
+        if (w < aw) base += x;
+        n_gt += x;
+      }
       if (n_gt <= (uint32_t)kListCap) {
-        uint32_t pa = gbase + ia - ca, pb = gbase + ta + ib - cb;
+        uint32_t pa = base + ia - ca, pb = base + ta + ib - cb;
         for (uint32_t m = ma; m; m &= m - 1) sh.list[pa++] = row_of(t0 + ga * 32 + __ffs(m) - 1);
         for (uint32_t m = mb; m; m &= m - 1) sh.list[pb++] = row_of(t0 + gb * 32 + __ffs(m) - 1);
         named_sync(kBarAtt, kAttThreads);  // the list of certain rows is complete
-        DS_TRACE_AT(1, 9);
         // batches of 8 list positions handed out by a shared cursor: batches
         // below nb1 are certain rows; the selected candidates follow from
         // position 8 * nb1 once the selection warps raise the flag
@@ -1175,7 +1148,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
             cp_async16(dst + kBatch * ROWB, vp + off, rv ? 16 : 0);
           }
         };
-        wait_keys_free();  // the ring stages alias this warp's share of the keys
         int nv_cur = 0, stg = 0;
         int cur = grab(nv_cur);
         if (cur >= 0) issue(cur, nv_cur, 0);
@@ -1195,8 +1167,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         }
         cp_async_wait<0>();
       } else {  // more certain rows than one list: rounds
-        wait_keys_free();
-        named_sync(kBarAtt, kAttThreads);  // (every warp has read wtot)
+        named_sync(kBarAtt, kAttThreads);
         run_rows([&](int g) { return sh.gtm[g]; }, false);
       }
       DS_TRACE_AT(1, 4);
@@ -1209,9 +1180,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         named_sync(kBarAtt, kAttThreads);
         run_rows([&](int g) { return sh.selm[g]; }, true);
       }
-    } else {  // the tail still scans the keys in this buffer: wait (every mark is in selm by then), then all rows
-      wait_keys_free();
-      named_sync(kBarAtt, kAttThreads);  // (every warp has read wtot)
+    } else {  // the tail still scans the keys in this buffer: wait, then all rows
+      named_sync(kBarDone, kThreads);
       run_rows([&](int g) { return sh.gtm[g] | sh.selm[g]; }, true);
     }
     DS_TRACE_AT(1, 5);

@@ -99,10 +99,6 @@ def report1():
         if ok.any():
             prev = s_
 report(2, ["start", "rowids", "loop done", "cluster sync", "merged"])
-report(1, ["start", "streamed", "split", "tail done", "gt rows done", "all rows", "merged"])
-# slots: 12 prologue end, 13 stream end (thread 0), 1 streams synced, 7 D1 known, 2 role split,
-# 8 gtm published (attention), 9 certain-row list built, 14 / 15 selection warp 0: split / eqm + candidates done
-report_slots(1, [(0, 12, "prologue"), (12, 13, "stream t0"), (13, 1, "stream sync"), (1, 7, "D1 boundary"),
-                 (2, 8, "gt scan"), (8, 9, "row list"), (2, 14, "sel split"), (14, 15, "eq scan+cand"),
-                 (15, 3, "tail"), (2, 3, "split->tail done"), (9, 4, "certain gathers"), (5, 10, "partials"),
-                 (10, 11, "weights"), (11, 6, "outputs")])
+report(1, ["start", "streamed", "masks", "tail done", "gt rows done", "all rows", "merged"])
+report_slots(1, [(0, 12, "prologue"), (12, 13, "stream t0"), (13, 1, "stream sync"), (1, 7, "D1 boundary"), (7, 8, "mask loop w0"), (8, 9, "cand gather w0"), (9, 2, "sync"),
+                 (2, 3, "tail"), (2, 14, "tail: level 2"), (14, 15, "tail: members"), (15, 3, "tail: rank+list"), (5, 10, "partials"), (10, 11, "weights"), (11, 6, "outputs")])
