@@ -419,7 +419,8 @@ __global__ void __launch_bounds__(kAttnThreads) attn_simt_kernel(AttnParams p) {
 }
 
 // ====================================================================
-// 16-bit path: TMA bulk row gathers + tensor-core QK and PV.
+// 16-bit path: cp.async row gathers + tensor-core QK and PV (TMA measured,
+// not faster: profiles/r2_tma_gather.md).
 //
 // Per warp and batch of 16 rows: the 256-B K and V rows are copied with
 // cp.async in 16-B chunks (one warp instruction = 512 B) into a padded stage

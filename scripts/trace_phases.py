@@ -102,3 +102,4 @@ report(2, ["start", "rowids", "loop done", "cluster sync", "merged"])
 report(1, ["start", "streamed", "masks", "tail done", "gt rows done", "all rows", "merged"])
 report_slots(1, [(0, 12, "prologue"), (12, 13, "stream t0"), (13, 1, "stream sync"), (1, 7, "D1 boundary"), (7, 8, "mask loop w0"), (8, 9, "cand gather w0"), (9, 2, "sync"),
                  (2, 3, "tail"), (2, 14, "tail: level 2"), (14, 15, "tail: members"), (15, 3, "tail: rank+list"), (5, 10, "partials"), (10, 11, "weights"), (11, 6, "outputs")])
+report_slots(2, [(0, 1, "sample sync")])  # fused decode, high-mask threshold (kind 2's slots borrowed)
