@@ -188,7 +188,11 @@ __device__ __forceinline__ uint32_t cluster_sum(int nch, F &&load) {
   return s;
 }
 
-template <typename T, int R, int D, bool CL>  // CL: a cluster of CTAs per unit
+// CL: a cluster of CTAs per unit.  PLAIN: the 16-bit label and the group-sum
+// reading fixed at compile time (the serving variant: the label-format / GQA
+// branches are compiled out, so its code is compact -- the serial phases
+// between the streams are otherwise slowed by instruction-cache misses)
+template <typename T, int R, int D, bool CL, bool PLAIN>
 __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   using GE = Geo<D>;
   constexpr int ROWB = GE::ROWB, CHN = GE::CHN, STAGE = GE::STAGE;
@@ -205,9 +209,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     else return ptr;
   };
   const CacheView &c = p.c;
+  const bool lq4 = !PLAIN && c.lq4, lnone = !PLAIN && c.lnone;     // label format (R16 / Table 4)
+  const int greduce = PLAIN ? (int)DS_GROUP_SUM : (int)c.greduce;  // GQA reading (R3 / R17)
   // a unit is one (b, KV head) -- or one (b, query head) for DS_GROUP_PER_HEAD
   // (reading R17: each query head selects on its own over its KV head's data)
-  const bool perh = c.greduce == DS_GROUP_PER_HEAD;
+  const bool perh = greduce == DS_GROUP_PER_HEAD;
   const int unit = blockIdx.y;
   const int nuh = perh ? c.Hq : c.Hkv;  // units per sequence
   const int b = unit / nuh, hu = unit - (unit / nuh) * nuh;
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
           if (v < CHN) reinterpret_cast<uint4 *>((T *)c.k_pool + dst)[v] = reinterpret_cast<const uint4 *>(kr)[v];
           else reinterpret_cast<uint4 *>((T *)c.v_pool + dst)[v - CHN] = reinterpret_cast<const uint4 *>(vr)[v - CHN];
         }
-        if (!c.lq4 && !c.lnone) {
+        if (!lq4 && !lnone) {
           T *lab = (T *)c.label + (((size_t)b * c.Hkv + h) * c.Smax + pn) * c.r;
           for (int j = lane; j < c.r; j += 32) lab[j] = kr[Ch[j]];
         }
@@ -276,13 +282,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   const int maxloc = max(0, min(p.chunk, c.Smax - t0));
   constexpr bool kVec16 = R > 0 && R * sizeof(T) == 16;  // one 16-B label row per token
   constexpr int U = kUnroll;
-  const bool q4v = R == 8 && c.lq4 && (c.Smax & 3) == 0;  // 16-B code / 8-B scale vectors of 4 tokens
+  const bool q4v = R == 8 && lq4 && (c.Smax & 3) == 0;  // 16-B code / 8-B scale vectors of 4 tokens
   // one register array for both label formats (int4: codes of two groups in
   // pv[0..1], their scales in pv[2])
   uint4 pv[U];
   bool pre = false;
-  if (c.lnone || c.greduce == DS_GROUP_MAX) {
-  } else if (!c.lq4) {
+  if (lnone || greduce == DS_GROUP_MAX) {
+  } else if (!lq4) {
     if constexpr (kVec16) {
       pre = tid + (U - 1) * kThreads < maxloc;
       if (pre) {
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   int32_t *btc = reinterpret_cast<int32_t *>(sh.cand);
   const int pg0 = t0 / c.P;
   const int npg = nloc > 0 ? (t0 + nloc - 1) / c.P - pg0 + 1 : 0;
-  const bool btc_ok = c.lnone && npg <= (int)(sizeof(sh.cand) / 4);
+  const bool btc_ok = lnone && npg <= (int)(sizeof(sh.cand) / 4);
   if (btc_ok)
     for (int i = tid; i < npg; i += kThreads) btc[i] = __ldg(c.block_table + (size_t)b * c.maxp + pg0 + i);
   cp_async_wait<0>();  // this thread's part of the query tile
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   auto qtile = [&](int g, int ch) {  // q[g][ch] from the swizzled tile
     return Elem<T>::to_f(*reinterpret_cast<const T *>(sh.qt + g * ROWB + swz(g, ch >> 3) + (ch & 7) * 2));
   };
-  const bool gmax = c.greduce == DS_GROUP_MAX;
+  const bool gmax = greduce == DS_GROUP_MAX;
   if (gmax) {  // R17: per-head query labels q_g[C[j]] at qlab[g * r + j]
     for (int i = tid; i < G * r; i += kThreads) {
       const int g = i / r, j = i - (i / r) * r;
@@ -378,17 +384,17 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     // R17: s_hat[t] = max_g (fma chain of q_g[C[j]] * L[t][j]) -- a plain
     // loop (diagnostic variant), every label format
     for (int i = tid; i < nloc; i += kThreads) {
-      const T *kr = c.lnone ? krow(t0 + i) : nullptr;
+      const T *kr = lnone ? krow(t0 + i) : nullptr;
       float m = -INFINITY;
       for (int g = 0; g < G; ++g) {
         const float *qv = sh.qlab + g * r;
         float s;
-        if (c.lq4) {
+        if (lq4) {
           s = q4_score<T>(cod + (size_t)i * c.rb, scl[i], qv, r);
         } else {
           s = 0.0f;
           for (int j = 0; j < r; ++j)
-            s = fmaf(qv[j], Elem<T>::to_f(c.lnone ? kr[c.C[(size_t)h * c.r + j]] : lab[(size_t)i * r + j]), s);
+            s = fmaf(qv[j], Elem<T>::to_f(lnone ? kr[c.C[(size_t)h * c.r + j]] : lab[(size_t)i * r + j]), s);
         }
         m = fmaxf(m, s);
       }
@@ -396,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       keys[i] = k0;
       DS_HIST_ADD(&sh.h1[k0 >> kSh1]);
     }
-  } else if (c.lnone) {
+  } else if (lnone) {
     // no label cache (the Table 4 ablation): the r channels are
     // read straight from each token's paged K row -- 2-byte reads scattered
     // over the 256-B row, one DRAM sector or more per channel
@@ -433,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       keys[i] = k0;
       DS_HIST_ADD(&sh.h1[k0 >> kSh1]);
     }
-  } else if (c.lq4) {
+  } else if (lq4) {
     // 4-bit label (reading R16): ceil(r/2) code bytes + one scale per
     // token; s_hat = (fma chain of q_label[j] * c_j) * s
     int i0 = tid;
@@ -512,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   const int pnew = p.k_new ? sh.newpos : -1;
   if (pnew >= t0 && pnew < t0 + nloc) {  // fused append: the new token's key from the values written
     if (tid == 0) {
-      if (c.lq4) {  // R16, the arithmetic of append_row_warp: codes replace the values in newlab
+      if (lq4) {  // R16, the arithmetic of append_row_warp: codes replace the values in newlab
         float a = 0.0f;
         for (int j = 0; j < r; ++j) a = fmaxf(a, fabsf(sh.newlab[j]));
         T st = Elem<T>::from_f(a == 0.0f ? 1.0f : a / 7.0f);
@@ -530,13 +536,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
           ((T *)c.label_scale)[lr] = st;
         }
       }
-      const bool gm = c.greduce == DS_GROUP_MAX;
+      const bool gm = greduce == DS_GROUP_MAX;
       float sc = -INFINITY;
       for (int g = 0; g < (gm ? G : 1); ++g) {
         const float *qv = sh.qlab + (gm ? g * r : 0);
         float acc = 0.0f;
         for (int j = 0; j < r; ++j) acc = fmaf(qv[j], sh.newlab[j], acc);
-        if (c.lq4) acc = acc * sh.newscale;
+        if (lq4) acc = acc * sh.newscale;
         sc = gm ? fmaxf(sc, acc) : acc;
       }
       const int i = pnew - t0;
@@ -618,22 +624,33 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     } else {
       // digit1 > D1 (>= D1 taken whole) <=> key >= gthr; digit1 == D1 <=>
       // key - (D1 << 20) < 2^20 (never, when D1 is taken whole)
-      const uint32_t gthr = (whole1 ? D1 : D1 + 1) << kSh1;  // (wraps to 0 for D1 = 4095, not whole:)
-      const bool gnone = !whole1 && D1 == (uint32_t)(kD1 - 1);  // nothing lies above the top digit
-      const uint32_t elo = D1 << kSh1, ewid = whole1 ? 0u : (1u << kSh1);
-      for (int base = w0; base < w1; base += 128) {
-        uint32_t kk[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) kk[e] = keys[base + 32 * e + lane];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t mg = __ballot_sync(0xffffffffu, !gnone && kk[e] >= gthr);
-          const uint32_t me = __ballot_sync(0xffffffffu, kk[e] - elo < ewid);
-          if (lane == e) {
-            sh.gtm[(base >> 5) + e] = mg;
-            sh.eqm[(base >> 5) + e] = me;
-          }
-        }
+      // (D1 = 4095 not taken whole: nothing lies above the top digit; the
+      // all-ones threshold admits no finite score's key, R6)
+      uint32_t gthr = !whole1 && D1 == (uint32_t)(kD1 - 1) ? 0xffffffffu : (whole1 ? D1 : D1 + 1) << kSh1;
+      uint32_t elo = D1 << kSh1, ewid = whole1 ? 0u : (1u << kSh1);
+      // (opaque copies: the compiler would otherwise split the ewid = 0 case
+      // into extra predicate logic and re-materialise D1 per group)
+      asm("mov.b32 %0, %0;" : "+r"(gthr));
+      asm("mov.b32 %0, %0;" : "+r"(elo));
+      asm("mov.b32 %0, %0;" : "+r"(ewid));
+      // this warp's <= 32 groups: lane gi keeps group gi's two masks (one
+      // store each at the end), the loop body is a load, two ballots and two
+      // selects per group -- the pass is bound by the ALU/FMA pipes (2 cycles
+      // per warp instruction each) with 32 warps per SM, ~2.4 us on c3
+      static_assert(kMaxS / 32 / kWarps <= 32, "one mask word per lane");
+      const int g0 = w0 >> 5, ng = (w1 - w0 + 31) >> 5;
+      uint32_t ga = 0u, ea = 0u;
+#pragma unroll 8
+      for (int gi = 0; gi < ng; ++gi) {
+        const uint32_t key = keys[(g0 + gi) * 32 + lane];
+        const uint32_t mg = __ballot_sync(0xffffffffu, key >= gthr);
+        const uint32_t me = __ballot_sync(0xffffffffu, key - elo < ewid);
+        ga = lane == gi ? mg : ga;
+        ea = lane == gi ? me : ea;
+      }
+      if (lane < ng) {
+        sh.gtm[g0 + lane] = ga;
+        sh.eqm[g0 + lane] = ea;
       }
       __syncwarp();
       DS_TRACE_AT(1, 8);
@@ -1306,15 +1323,15 @@ static size_t smem_bytes(int chunk) {
   return sizeof(Sh) + region;
 }
 
-template <typename T, int R, int D, bool CL>
+template <typename T, int R, int D, bool CL, bool PLAIN>
 static cudaError_t launch_cl(const ds_cache *c, const FusedParams &p, int nch, cudaStream_t st) {
   const size_t smem = smem_bytes<T, R, D>(p.chunk);
   static PerDeviceOnce once;
   const cudaError_t attr = once([] {
-    cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, R, D, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kFusedMaxSmem);
+    cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, R, D, CL, PLAIN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedMaxSmem);
     if (e == cudaSuccess && CL)
-      e = cudaFuncSetAttribute(decode_kernel<T, R, D, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      e = cudaFuncSetAttribute(decode_kernel<T, R, D, CL, PLAIN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return e;
   });
   if (attr != cudaSuccess) return attr;
@@ -1333,12 +1350,16 @@ static cudaError_t launch_cl(const ds_cache *c, const FusedParams &p, int nch, c
   a[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = CL ? a : a + 1;  // no cluster attribute for one CTA per unit
   cfg.numAttrs = CL ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, decode_kernel<T, R, D, CL>, p);
+  return cudaLaunchKernelEx(&cfg, decode_kernel<T, R, D, CL, PLAIN>, p);
 }
 
 template <typename T, int R, int D>
 static cudaError_t launch_t(const ds_cache *c, const FusedParams &p, int nch, cudaStream_t st) {
-  return nch > 1 ? launch_cl<T, R, D, true>(c, p, nch, st) : launch_cl<T, R, D, false>(c, p, nch, st);
+  // the serving variant (16-bit label, group sum) has its own compact instance
+  const bool plain = R > 0 && c->label_format == DS_LABEL_NATIVE && c->group_reduce == DS_GROUP_SUM;
+  if (nch > 1)
+    return plain ? launch_cl<T, R, D, true, true>(c, p, nch, st) : launch_cl<T, R, D, true, false>(c, p, nch, st);
+  return plain ? launch_cl<T, R, D, false, true>(c, p, nch, st) : launch_cl<T, R, D, false, false>(c, p, nch, st);
 }
 
 // Can a cluster of nch CTAs (1024 threads, ~200 KB of shared memory each) be
@@ -1349,10 +1370,10 @@ static bool cluster_fits_t(int nch, int chunk) {
   if (nch <= 8) return true;
   static PerDeviceOnce once;
   if (once([] {
-        cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, R, D, true>,
+        cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, R, D, true, false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedMaxSmem);
         if (e == cudaSuccess)
-          e = cudaFuncSetAttribute(decode_kernel<T, R, D, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+          e = cudaFuncSetAttribute(decode_kernel<T, R, D, true, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         return e;
       }) != cudaSuccess)
     return false;
@@ -1368,7 +1389,7 @@ static bool cluster_fits_t(int nch, int chunk) {
   cfg.attrs = a;
   cfg.numAttrs = 1;
   int nclusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&nclusters, decode_kernel<T, R, D, true>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&nclusters, decode_kernel<T, R, D, true, false>, &cfg) != cudaSuccess) {
     cudaGetLastError();  // clear the sticky-free error of the query
     return false;
   }
