@@ -6,10 +6,15 @@ A step = one decode step of the whole hot path over L resident layer caches:
 per layer a0 (the current token's K/V + label row) + a1..a5, as one ds_decode_attention_append.
 Workload at N=1: c3 (Llama-3-8B GQA, B=16, H_q=32, H_kv=8, d=128, S=32768,
 r=8, k=2048, bf16) -- the config BASELINE.json's metric names (S=32K, 1-8 B200).
-N>1 (torchrun, one rank per GPU): weak scaling, every rank runs its own c3
-batch (independent units, no data-path collective); --mode allgather instead
-shards c3's KV heads over the ranks and all-gathers the head outputs over NCCL
-(strong scaling, north_star's variant).
+N>1 (torchrun, one rank per GPU), default --mode allgather (north_star's
+multi-GPU variant): the config's KV heads are split into
+contiguous slices, rank r owning KV heads [r H_kv/N, (r+1) H_kv/N) with their
+G query heads and all B sequences (c3 at N=8: one KV head per rank; c4 at N=8:
+one KV head and all 64 sequences), and each layer's head outputs are
+all-gathered over NCCL inside the captured step (the path's only exchange).
+Strong scaling: the total work is the config's.  The kernel-only step (same
+graph without the collective) is reported beside it.  --mode weak instead runs
+a full independent batch per rank (no collective).
 
 value = algorithmic HBM bytes (label S*r*e + gathered K/V 2*k*d*e per unit,
 SURVEY 8(d)) of all layers of all ranks / max-over-ranks device time, GB/s.
@@ -54,9 +59,15 @@ def parse():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--structure", default="iid", choices=["iid", "clustered"])
+    ap.add_argument("--pages", default="random", choices=["random", "identity"],
+                    help="physical page order of each sequence (random: the headline, worst DRAM locality)")
+    ap.add_argument("--no-dense-refs", action="store_true",
+                    help="skip the library dense references (torch SDPA, flashinfer trtllm-gen)")
     ap.add_argument("--label", default="native", choices=["native", "int4"],
                     help="label cache storage: K's dtype (north_star's byte model) or 4-bit (P:171, f2)")
-    ap.add_argument("--mode", default="weak", choices=["weak", "allgather"])
+    ap.add_argument("--mode", default="allgather", choices=["weak", "allgather"],
+                    help="N>1: allgather = KV-head shards + NCCL all-gather of head outputs (strong scaling), "
+                         "weak = a full independent batch per rank")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -167,6 +178,7 @@ class Dist:
         self.pg = None
 
     def init(self, backend):
+        self.backend = backend
         if self.world > 1:
             import torch.distributed as dist
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -175,7 +187,7 @@ class Dist:
 
     def barrier(self):
         if self.pg:
-            if torch.cuda.is_available():
+            if torch.cuda.is_available() and getattr(self, "backend", "nccl") == "nccl":
                 self.pg.barrier(device_ids=[self.local])
             else:
                 self.pg.barrier()
@@ -183,7 +195,7 @@ class Dist:
     def max(self, x: float) -> float:
         if not self.pg:
             return x
-        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        dev = "cuda" if torch.cuda.is_available() and getattr(self, "backend", "nccl") == "nccl" else "cpu"
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
@@ -194,8 +206,9 @@ class Dist:
 
 
 def shard_plan(cfg: synth.Config, world: int, rank: int, mode: str):
-    """Units a rank owns.  weak: a full cfg batch per rank (seeded by rank).
-    allgather: a contiguous slice of KV heads (and their G query heads)."""
+    """Units a rank owns and the first KV head of its slice.  weak: a full cfg
+    batch per rank (seeded by rank).  allgather: a contiguous slice of KV heads
+    (and their G query heads) of every sequence."""
     if mode == "weak" or world == 1:
         return cfg, 0
     try:
@@ -203,6 +216,19 @@ def shard_plan(cfg: synth.Config, world: int, rank: int, mode: str):
     except ValueError as e:
         raise SystemExit(f"--mode allgather: {e}")
     return cfg.with_(Hkv=h1 - h0, Hq=cfg.G * (h1 - h0)), h0
+
+
+def make_step(layers, call_layer, pg=None, gathered=None):
+    """One decode step over the resident layers: call_layer(layer) runs the
+    hot path of one layer (one ds_decode_attention_append launch); with a
+    process group, each layer's head outputs are then all-gathered into
+    gathered[i] ([world][B][Hq/world][d]), the path's only exchange."""
+    def step():
+        for i, ly in enumerate(layers):
+            call_layer(ly)
+            if gathered is not None:
+                shard.allgather_heads(pg, ly["out"], gathered[i])
+    return step
 
 
 # ------------------------------------------------------------------ clocks
@@ -285,12 +311,12 @@ class Clocks:
 
 
 # ----------------------------------------------------------- our GPU arm
-def build_layers(cfg, L, rank, structure, device, label="native"):
+def build_layers(cfg, L, rank, structure, device, label="native", identity_pages=False):
     import paper_2408_07092_b200 as ds
     layers = []
     for l in range(L):
         seed = cfg.seed_base + 97 * rank + l
-        lay = synth.make_layer(cfg, seed, device=device, structure=structure)
+        lay = synth.make_layer(cfg, seed, device=device, structure=structure, identity_pages=identity_pages)
         Qc, Kc = synth.make_calibration(cfg, n=512, seed=seed, device=device)
         C = ds.ds_calibrate_channels(Qc, Kc, cfg.Hkv, cfg.r)            # offline, untimed
         cache = ds.LayerCache.allocate(cfg.B, cfg.Hq, cfg.Hkv, cfg.d, cfg.S, cfg.r, synth.DTYPES[cfg.dtype],
@@ -313,16 +339,21 @@ def time_graph(fn, steps, warmup, dist, stream, sampler=None):
     """Capture fn() in a CUDA graph, replay W times, then time exactly K replays
     with events on the capture stream (barrier + sync on both sides).
     sampler(): started right before the timed replays, stopped right after;
-    its result is returned as a third value."""
+    its result is returned as a third value.  If the capture fails (a
+    collective the backend cannot capture), fn itself is timed the same way
+    and the returned graph is None."""
     with torch.cuda.stream(stream):
-        fn()                                   # eager warm-up (attribute setup, allocator)
+        fn()                                   # eager warm-up (attribute setup, allocator, communicator)
     torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=stream):
-        fn()
+    g, run = None, fn
+    if getattr(dist, "backend", "nccl") != "gloo":  # (gloo collectives cannot be captured: eager)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+        run = g.replay
     with torch.cuda.stream(stream):           # replay() launches on the current stream
         for _ in range(warmup):
-            g.replay()
+            run()
         torch.cuda.synchronize()
         dist.barrier()
         torch.cuda.synchronize()
@@ -330,7 +361,7 @@ def time_graph(fn, steps, warmup, dist, stream, sampler=None):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(steps):
-            g.replay()
+            run()
         e1.record(stream)
         torch.cuda.synchronize()
         sampled = smp.stop() if smp else None
@@ -346,9 +377,15 @@ def run_ours(args, dist):
     torch.cuda.set_device(dev)
     full = synth.CONFIGS[args.config]
     cfg, h0 = shard_plan(full, dist.world, dist.rank, args.mode)
-    L = args.layers
     hbm_peak, peak_src = peaks()
-    layers = build_layers(cfg, L, dist.rank if args.mode == "weak" else 0, args.structure, dev, args.label)
+    # the layers swept per step must cover >= 4x the L2, so no
+    # layer's bytes are still cached when it comes round again
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    bytes_layer = ledger.layer_bytes_alg(cfg, args.label)
+    L = max(args.layers, -(-4 * l2 // bytes_layer))
+    layers = build_layers(cfg, L, dist.rank if args.mode == "weak" else 0, args.structure, dev, args.label,
+                          identity_pages=args.pages == "identity")
+    assert L * bytes_layer >= 4 * l2, "swept footprint below 4x L2"
     k = cfg.k
     ws = ds.workspace(ds.ds_decode_workspace_size(layers[0]["cache"], k), dev)
     stream = torch.cuda.Stream(dev)
@@ -360,14 +397,13 @@ def run_ours(args, dist):
     sp = ctypes.c_void_p(stream.cuda_stream)
     P = ctypes.c_void_p
 
-    def step():  # a0 + a1..a5 per layer: ds_decode_attention_append (one launch on the single-kernel path)
-        for i, ly in enumerate(layers):
-            ds._check(lib.ds_decode_attention_append(ctypes.byref(ly["cs"]), P(ly["k_new"].data_ptr()),
-                                                     P(ly["v_new"].data_ptr()), P(ly["pos"].data_ptr()),
-                                                     P(ly["q"].data_ptr()), k, P(ly["out"].data_ptr()), None,
-                                                     P(ws.data_ptr()), ws.numel(), sp), "append+decode")
-            if gathered is not None:
-                shard.allgather_heads(dist.pg, ly["out"], gathered[i])   # the path's one exchange step
+    def call_layer(ly):  # a0 + a1..a5 of one layer: ds_decode_attention_append (one launch)
+        ds._check(lib.ds_decode_attention_append(ctypes.byref(ly["cs"]), P(ly["k_new"].data_ptr()),
+                                                 P(ly["v_new"].data_ptr()), P(ly["pos"].data_ptr()),
+                                                 P(ly["q"].data_ptr()), k, P(ly["out"].data_ptr()), None,
+                                                 P(ws.data_ptr()), ws.numel(), sp), "append+decode")
+
+    step = make_step(layers, call_layer, dist.pg, gathered)
 
     def decode_only_layer(ly):
         ds._check(lib.ds_decode_attention(ctypes.byref(ly["cs"]), P(ly["q"].data_ptr()), k, P(ly["out"].data_ptr()),
@@ -384,6 +420,10 @@ def run_ours(args, dist):
     ms_total, g_step, clocks = time_graph(step, args.steps, args.warmup, dist, stream,
                                           sampler=lambda: Clocks(dist.local, cpath))
     ms_step = dist.max(ms_total / args.steps)
+    ms_kernel_step = None
+    if gathered is not None:  # the same step without the collective: kernel-only time
+        ms_k, _ = time_graph(make_step(layers, call_layer), args.steps, 2, dist, stream)
+        ms_kernel_step = dist.max(ms_k / args.steps)
 
     # dominant launch group for the roofline: ds_decode_attention alone over the same layers
     ms_dec_total, g_dec = time_graph(decode_only, args.steps, 2, dist, stream)
@@ -393,8 +433,8 @@ def run_ours(args, dist):
     # torch.profiler, three more replays each), and of one decode launch in
     # isolation after an L2 flush
     with torch.cuda.stream(stream):
-        ks_step = kernel_trace(g_step.replay, reps=3)
-        ks_dec = kernel_trace(g_dec.replay, reps=3)
+        ks_step = kernel_trace(g_step.replay if g_step is not None else step, reps=3)
+        ks_dec = kernel_trace(g_dec.replay if g_dec is not None else decode_only, reps=3)
         flush = torch.ones(256 << 20, dtype=torch.bfloat16, device=dev)
 
         def iso():
@@ -405,7 +445,6 @@ def run_ours(args, dist):
         ks_iso = [x for x in kernel_trace(iso, reps=10) if "decode_kernel" in x["name"]]
         del flush
 
-    bytes_layer = ledger.layer_bytes_alg(cfg, args.label)
     n_ranks = dist.world
     total_bytes = bytes_layer * L * (n_ranks if args.mode == "weak" else 1) if args.mode == "weak" else \
         ledger.layer_bytes_alg(full, args.label) * L
@@ -419,10 +458,13 @@ def run_ours(args, dist):
         "config": {"workload": f"{full.name}: B={full.B} Hq={full.Hq} Hkv={full.Hkv} d={full.d} S={full.S} "
                                f"r={full.r} k={full.k} {full.dtype}" + (" label=int4" if args.label == "int4" else ""),
                    "label": args.label, "layers_resident": L,
-                   "structure": args.structure, "page_size": cfg.page_size,
+                   "structure": args.structure, "page_size": cfg.page_size, "page_order": args.pages,
                    "parallelism": (f"dp{n_ranks}" if args.mode == "weak" else f"kv-head-shard{n_ranks}+allgather"),
-                   "l2": f"inputs > L2: each step touches {L} x {bytes_layer / 2**20:.0f} MiB of distinct layer caches"},
+                   "l2": f"inputs > L2: each step touches {L} x {bytes_layer / 2**20:.1f} MiB of distinct layer caches "
+                         f"= {L * bytes_layer / l2:.1f} x the {l2 / 2**20:.0f} MiB L2 (>= 4x asserted)"},
         "us_per_layer": round(us_layer, 3),
+        "kernel_only_ms_per_step": round(ms_kernel_step, 5) if ms_kernel_step is not None else None,
+        "step_graph_captured": g_step is not None,
         "tokens_per_s_attn": round(full.B * (n_ranks if args.mode == "weak" else 1) * 1e6 / (us_layer * 32), 1),
         "bytes_alg_per_layer": bytes_layer,
     }
@@ -487,9 +529,17 @@ def run_ours(args, dist):
         res["speedup_vs_dense"] = round(us_dense / us_decode, 3)
         res["byte_ratio_ceiling"] = round(ledger.byte_ratio_ceiling(cfg, args.label), 3)
         del dws
+        if not args.no_dense_refs:
+            refs = dense_references(cfg, layers, args, dist, stream)
+            refs["ours_dense_flash_decode"] = {"us_per_layer": round(us_dense, 3), "gbs": res["dense_gbs"]}
+            res["dense_refs"] = refs
+            fastest = min((v["us_per_layer"] for v in refs.values() if "us_per_layer" in v), default=None)
+            if fastest:
+                res["fastest_dense_us_per_layer"] = round(fastest, 3)
+                res["speedup_vs_fastest_dense"] = round(fastest / us_decode, 3)
 
     if not args.no_e2e:
-        res["e2e"] = e2e(args, dist, layers, ws, k, stream, cfg)
+        res["e2e"] = e2e(args, dist, layers, ws, k, stream, cfg, gathered is not None)
     if args.extra and dist.world == 1:
         res["extra"] = extra_configs(args)
     del layers
@@ -499,17 +549,73 @@ def run_ours(args, dist):
     return res
 
 
-def e2e(args, dist, layers, ws, k, stream, cfg):
+def dense_references(cfg, layers, args, dist, stream):
+    """Dense decode attention over every token, by library kernels on the
+    same shapes: torch SDPA on contiguous K/V [B][H_kv][S][d]
+    (the paper's baseline; GQA through enable_gqa) and flashinfer's
+    trtllm-gen decode kernel on our paged pools (HND layout, the same block
+    tables).  Each is timed like ours (CUDA graph over the resident layers,
+    events, max over ranks); a reference that cannot run reports its error."""
+    import math
+
+    import torch.nn.functional as F
+    out = {}
+    L = len(layers)
+    dbytes = ledger.layer_bytes_dense(cfg)
+    steps = max(3, args.steps // 4)
+    dev = layers[0]["q"].device
+    try:
+        kv = [(torch.randn((cfg.B, cfg.Hkv, cfg.S, cfg.d), device=dev, dtype=layers[0]["q"].dtype),
+               torch.randn((cfg.B, cfg.Hkv, cfg.S, cfg.d), device=dev, dtype=layers[0]["q"].dtype)) for _ in range(L)]
+        qs = [ly["q"].view(cfg.B, cfg.Hq, 1, cfg.d) for ly in layers]
+
+        def sdpa():
+            for i in range(L):
+                F.scaled_dot_product_attention(qs[i], kv[i][0], kv[i][1], enable_gqa=cfg.G > 1)
+        ms, _ = time_graph(sdpa, steps, 2, dist, stream)
+        us = dist.max(ms / steps) * 1e3 / L
+        out["torch_sdpa"] = {"us_per_layer": round(us, 3), "gbs": round(dbytes / (us * 1e-6) / 1e9, 1),
+                             "kv": "contiguous [B][H_kv][S][d]"}
+        del kv
+        torch.cuda.empty_cache()
+    except Exception as e:
+        out["torch_sdpa"] = {"error": f"{type(e).__name__}: {str(e)[:160]}"}
+    try:
+        from flashinfer.decode import trtllm_batch_decode_with_kv_cache
+        wsb = torch.zeros(256 << 20, dtype=torch.uint8, device=dev)
+        outs = [torch.empty_like(ly["q"]) for ly in layers]
+        scale = 1.0 / math.sqrt(cfg.d)
+
+        def fi():
+            for i, ly in enumerate(layers):
+                c = ly["cache"]
+                trtllm_batch_decode_with_kv_cache(ly["q"], (c.k_pool, c.v_pool), wsb, c.block_table, c.seq_lens,
+                                                  cfg.S, bmm1_scale=scale, bmm2_scale=1.0, out=outs[i],
+                                                  kv_layout="HND", backend="trtllm-gen")
+        ms, _ = time_graph(fi, steps, 2, dist, stream)
+        us = dist.max(ms / steps) * 1e3 / L
+        out["flashinfer_trtllm_gen"] = {"us_per_layer": round(us, 3), "gbs": round(dbytes / (us * 1e-6) / 1e9, 1),
+                                        "kv": "our paged pools, HND, page 16"}
+        del wsb, outs
+    except Exception as e:
+        out["flashinfer_trtllm_gen"] = {"error": f"{type(e).__name__}: {str(e)[:160]}"}
+    return out
+
+
+def e2e(args, dist, layers, ws, k, stream, cfg, allgather=False):
     """Same metric through the public Python API with host buffers: per step the
     current token's q/k_new/v_new of every layer are copied from pinned host
-    memory and every layer's output is read back, inside the timed region."""
+    memory and every layer's output is read back, inside the timed region.
+    allgather: each layer's head outputs are all-gathered (every rank reads
+    back all heads)."""
     import paper_2408_07092_b200 as ds
     # the step's inputs (every layer's q, k_new, v_new) packed in one pinned
     # host buffer and one device buffer, so each step is one H2D copy, the
     # layer calls on views of it, and one D2H copy of all outputs
     srcs = [t for ly in layers for t in (ly["q"], ly["k_new"], ly["v_new"])]
     nin = [t.numel() * t.element_size() for t in srcs]
-    nout = [ly["out"].numel() * ly["out"].element_size() for ly in layers]
+    wmul = dist.world if allgather else 1
+    nout = [ly["out"].numel() * ly["out"].element_size() * wmul for ly in layers]
     h_in = torch.empty(sum(nin), dtype=torch.uint8).pin_memory()
     h_out = torch.empty(sum(nout), dtype=torch.uint8).pin_memory()
     d_in = torch.empty(sum(nin), dtype=torch.uint8, device=layers[0]["q"].device)
@@ -525,15 +631,45 @@ def e2e(args, dist, layers, ws, k, stream, cfg):
     for hv_, t in zip(views(h_in, srcs, nin), srcs):
         hv_.copy_(t.cpu())
     dq, dk, dvv = dv[0::3], dv[1::3], dv[2::3]
-    do = views(d_out, [ly["out"] for ly in layers], nout)
+    if allgather:
+        outs = [torch.empty((dist.world,) + tuple(ly["out"].shape), dtype=ly["out"].dtype) for ly in layers]
+        gat = views(d_out, outs, nout)
+        do = [torch.empty_like(ly["out"]) for ly in layers]
+    else:
+        do = views(d_out, [ly["out"] for ly in layers], nout)
     h2d, d2h = h_in.numel(), h_out.numel()
 
+    # per layer, its inputs (q, k_new, v_new: adjacent in the packed buffers)
+    # and its outputs, so the copies pipeline with the kernels: layer i waits
+    # only for its own H2D copy (on the h2d stream), and its D2H copy (on the
+    # d2h stream) runs while later layers compute
+    lin = [sum(nin[3 * i:3 * i + 3]) for i in range(len(layers))]
+    oin = [sum(lin[:i]) for i in range(len(layers))]
+    oout = [sum(nout[:i]) for i in range(len(layers))]
+    h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in layers]
+    ev_out = [torch.cuda.Event() for _ in layers]
+
     def one():
-        d_in.copy_(h_in, non_blocking=True)
+        cur = torch.cuda.current_stream()
+        h2d_s.wait_stream(cur)
+        d2h_s.wait_stream(cur)
+        with torch.cuda.stream(h2d_s):
+            for i in range(len(layers)):
+                d_in[oin[i]:oin[i] + lin[i]].copy_(h_in[oin[i]:oin[i] + lin[i]], non_blocking=True)
+                ev_in[i].record(h2d_s)
         for i, ly in enumerate(layers):
+            cur.wait_event(ev_in[i])
             ds.ds_decode_attention_append(ly["cache"], dk[i], dvv[i], ly["pos"], dq[i], k, out=do[i], ws=ws,
                                           cs=ly["cs"])
-        h_out.copy_(d_out, non_blocking=True)
+            if allgather:
+                shard.allgather_heads(dist.pg, do[i], gat[i])
+            ev_out[i].record(cur)
+            with torch.cuda.stream(d2h_s):
+                d2h_s.wait_event(ev_out[i])
+                h_out[oout[i]:oout[i] + nout[i]].copy_(d_out[oout[i]:oout[i] + nout[i]], non_blocking=True)
+        cur.wait_stream(h2d_s)
+        cur.wait_stream(d2h_s)
 
     def timed(run):
         with torch.cuda.stream(stream):
@@ -558,12 +694,16 @@ def e2e(args, dist, layers, ws, k, stream, cfg):
     ms_eager = timed(one)
     # the same calls and copies captured once with the package's CapturedStep
     # (one graph launch per step; the copies stay inside every replay)
-    cap = ds.CapturedStep(one, stream=stream)
-    ms = timed(cap.graph.replay)
+    if getattr(dist, "backend", "nccl") == "gloo":  # (one-GPU test mode: nothing to capture)
+        ms = ms_eager
+    else:
+        cap = ds.CapturedStep(one, stream=stream)
+        ms = timed(cap.graph.replay)
     return {"value": round(per_step / (ms / 1e3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 5),
-            "api": "paper_2408_07092_b200.CapturedStep over ds_decode_attention_append, one pinned H2D copy of the "
-                   "step's inputs and one D2H copy of its outputs",
+            "api": "paper_2408_07092_b200.CapturedStep over ds_decode_attention_append; per layer one pinned H2D "
+                   "copy of its inputs (h2d stream) and one D2H copy of its outputs (d2h stream), pipelined with "
+                   "the layers' kernels",
             "eager": {"value": round(per_step / (ms_eager / 1e3) / 1e9, 2), "ms_per_step": round(ms_eager, 5),
                       "api": "ds_decode_attention_append called per layer from Python"}}
 
@@ -631,10 +771,11 @@ def oracle_sample(cfg: synth.Config, n_seq: int, seed: int, label="native"):
     return sc, q, K, V, L, C, lay.seq_lens.numpy(), (q4 or {})
 
 
-def cpu_baseline(cfg: synth.Config, budget_s: float = 12.0, nthreads=None, label="native"):
+def cpu_baseline(cfg: synth.Config, budget_s: float = 12.0, nthreads=None, label="native", one_core_s: float = 5.0):
     """The oracle as it stands, on this host's cores, on a bounded sample of the
     same workload: whole sequences (all KV heads) of cfg, as many as fit the
-    time budget (pilot-timed)."""
+    time budget (pilot-timed); then the same oracle on ONE core over single
+    units (SURVEY 8(d) asks for both)."""
     import oracle
     nthreads = nthreads or os.cpu_count() or 1
     n_seq = max(1, -(-nthreads // cfg.Hkv))            # enough units to occupy every core
@@ -649,11 +790,26 @@ def cpu_baseline(cfg: synth.Config, budget_s: float = 12.0, nthreads=None, label
         oracle.decode_batch(q, K, V, L, C, sl, cfg.k, nthreads=nthreads, **q4)
     dt = time.perf_counter() - t
     units = sc.units * reps
-    bytes_ = units * ledger.unit_bytes_alg(cfg.S, cfg.d, cfg.r, cfg.k, cfg.elem, label)
+    ubytes = ledger.unit_bytes_alg(cfg.S, cfg.d, cfg.r, cfg.k, cfg.elem, label)
+    bytes_ = units * ubytes
+    # one core: the first sequence's first KV head, repeated within one_core_s
+    q1 = {kk: v[:1, :1] for kk, v in q4.items()}
+    args1 = (q[:1, :cfg.G], K[:1, :1], V[:1, :1], L[:1, :1], C[:1], sl[:1], cfg.k)
+    t = time.perf_counter()
+    oracle.decode_batch(*args1, nthreads=1, **q1)
+    p1 = time.perf_counter() - t
+    r1 = max(1, int(one_core_s / max(p1, 1e-3)))
+    t = time.perf_counter()
+    for _ in range(r1):
+        oracle.decode_batch(*args1, nthreads=1, **q1)
+    d1 = time.perf_counter() - t
     return {"value": round(bytes_ / dt / 1e9, 4), "unit": "GB/s", "cores": nthreads, "kind": "oracle",
             "sample": f"{reps} x {sc.B} sequences ({sc.units} units of {cfg.name}, S={cfg.S}, k={cfg.k}), "
                       f"Algorithm 1 in plain fp32 C, {dt:.1f} s",
-            "us_per_unit": round(dt / units * 1e6, 1)}
+            "us_per_unit": round(dt / units * 1e6, 1),
+            "one_core": {"value": round(r1 * ubytes / d1 / 1e9, 4), "unit": "GB/s", "cores": 1,
+                         "us_per_unit": round(d1 / r1 * 1e6, 1),
+                         "sample": f"{r1} x 1 unit of {cfg.name} on one thread, {d1:.1f} s"}}
 
 
 def run_reference(args, dist):
@@ -796,8 +952,12 @@ def main():
     if not torch.cuda.is_available():
         raise SystemExit("bench.py (ours) needs a CUDA device; there is no CPU fallback")
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    # DS_BENCH_ONE_GPU=1 (tests only): every rank on cuda:0 over gloo, to run
+    # the N>1 code path on a one-GPU box (no graph capture of the collective)
+    if os.environ.get("DS_BENCH_ONE_GPU") == "1":
+        dist.local = 0
     torch.cuda.set_device(dist.local)  # before the NCCL communicator is created
-    dist.init("nccl")
+    dist.init("gloo" if os.environ.get("DS_BENCH_ONE_GPU") == "1" else "nccl")
     res = run_offload(args, dist) if args.offload else run_ours(args, dist)
     if dist.rank == 0:
         print(json.dumps(res), flush=True)

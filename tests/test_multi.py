@@ -100,3 +100,59 @@ def test_allgather_world2_gloo_reassembles_single_process_output():
     ref = _oracle_outputs(lay, (0, CFG.Hkv))
     for rank, y, _, _ in res:
         assert np.array_equal(y, ref), f"rank {rank}: gathered output differs"
+
+
+def _bench_step_worker(rank, world, port, q):
+    """bench.py's N>1 path on CPU: shard_plan's KV-head slice, make_step's
+    per-layer call + all-gather (the oracle standing in for the kernel)."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import bench
+        cfg, h0 = bench.shard_plan(CFG, world, rank, "allgather")
+        layers = []
+        for l in range(2):
+            lay = synth.make_layer(CFG, 11 + l, device="cpu", seq_lens=[96, 70])
+            layers.append(dict(lay=lay, out=torch.empty((CFG.B, cfg.Hq, CFG.d))))
+
+        def call_layer(ly):
+            ly["out"].copy_(torch.from_numpy(_oracle_outputs(ly["lay"], (h0, h0 + cfg.Hkv))))
+        gathered = [torch.empty((world,) + tuple(ly["out"].shape)) for ly in layers]
+        bench.make_step(layers, call_layer, dist, gathered)()
+        q.put((rank, [shard.heads_from_gathered(g).numpy() for g in gathered], (cfg.Hkv, cfg.Hq, h0)))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, repr(e), None))
+
+
+def test_bench_step_world2_gloo_allgather_mode():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_bench_step_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    refs = [_oracle_outputs(synth.make_layer(CFG, 11 + l, device="cpu", seq_lens=[96, 70]), (0, CFG.Hkv))
+            for l in range(2)]
+    for rank, ys, shp in res:
+        assert not isinstance(ys, str), f"rank {rank} failed: {ys}"
+        assert shp == (CFG.Hkv // world, CFG.Hq // world, rank * CFG.Hkv // world)
+        for y, ref in zip(ys, refs):
+            assert np.array_equal(y, ref), f"rank {rank}: gathered step output differs"
+
+
+def test_shard_plan_modes():
+    import bench
+    c3 = synth.CONFIGS["c3"]
+    for world in (1, 2, 4, 8):
+        for rank in range(world):
+            cfg, h0 = bench.shard_plan(c3, world, rank, "allgather")
+            assert (cfg.Hkv, cfg.Hq, cfg.B, h0) == (8 // world, 32 // world, 16, rank * 8 // world)
+            assert bench.shard_plan(c3, world, rank, "weak") == (c3, 0)
+    c4 = synth.CONFIGS["c4"]
+    cfg, h0 = bench.shard_plan(c4, 8, 5, "allgather")
+    assert (cfg.Hkv, cfg.Hq, cfg.B, h0) == (1, 8, 64, 5)  # c4 at N=8: one KV head and all 64 sequences per rank
