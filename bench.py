@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--extra", action="store_true", help="also time c2 S=4K/16K/32K (reported under 'extra')")
+    ap.add_argument("--offload-layers", type=int, default=32,
+                    help="--offload: layers of pinned host K/V (capped by host memory)")
     ap.add_argument("--offload", action="store_true",
                     help="Double Sparsity-Offload pipeline on c5 (KV in pinned host memory); prints its own line")
     return ap.parse_args()
@@ -472,7 +474,7 @@ def run_ours(args, dist):
     n_dec = ds.ds_decode_launches(layers[0]["cache"], cfg.k)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{full.name}" + ("_int4" if args.label == "int4" else "") + ".json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and cfg == full:  # (the captured launch is the full config's)
         try:
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch_group")
         except Exception:
@@ -847,6 +849,55 @@ def run_reference(args, dist):
             "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def link_peaks(dev, nbytes: int = 1 << 30, reps: int = 3):
+    """Host-link ceilings in this run: pinned host -> device and device ->
+    pinned host cudaMemcpy of `nbytes` (copy engine), best of `reps`, GB/s."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    out = {}
+    for name, dst, src in (("h2d_gbs", d, h), ("d2h_gbs", h, d)):
+        best = float("inf")
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out[name] = round(nbytes / (best / 1e3) / 1e9, 2)
+    out["bytes"] = nbytes
+    del h, d
+    torch.cuda.empty_cache()
+    return out
+
+
+def _union(iv):
+    out = []
+    for a, b in sorted(iv):
+        if out and a <= out[-1][1]:
+            out[-1] = (out[-1][0], max(out[-1][1], b))
+        else:
+            out.append((a, b))
+    return out
+
+
+def _intersect(x, y):
+    out, i, j = [], 0, 0
+    while i < len(x) and j < len(y):
+        a, b = max(x[i][0], y[j][0]), min(x[i][1], y[j][1])
+        if a < b:
+            out.append((a, b))
+        if x[i][1] < y[j][1]:
+            i += 1
+        else:
+            j += 1
+    return out
+
+
+def _measure(iv):
+    return sum(b - a for a, b in _union(iv))
+
+
 def run_offload(args, dist):
     """f1: Double Sparsity-Offload on c5.  K/V pools live in pinned
     host memory; per layer l, the main stream attends over slot l % 2 (rows
@@ -858,7 +909,16 @@ def run_offload(args, dist):
     dev = torch.device("cuda", dist.local)
     torch.cuda.set_device(dev)
     cfg = synth.CONFIGS["c5"]
-    L = min(args.layers, 2)
+    # L = 32 (Llama-3-8B) layers of pinned host K/V (2 GiB each), or as many
+    # as half the available host memory holds
+    host_kv_layer = 2 * cfg.B * cfg.Hkv * cfg.S * cfg.d * cfg.elem
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 64 << 30
+    L = max(2, min(args.offload_layers, int(0.5 * avail // host_kv_layer)))
+    link = link_peaks(dev)
     layers = []
     for l in range(L):
         seed = cfg.seed_base + l
@@ -907,6 +967,15 @@ def run_offload(args, dist):
     ms = e0.elapsed_time(e1) / args.steps
     us_layer = ms * 1e3 / L
     link_bytes = cfg.B * cfg.Hkv * cfg.k * 2 * cfg.d * cfg.elem          # K+V rows per layer over the link
+    # overlap (CUPTI kernel activity over one more step): the share of the
+    # attention kernels' time that the side stream's prefetch kernels cover
+    ks = kernel_trace(lambda: step((args.warmup + args.steps) * L), reps=1)
+    pre = [(k["ts"], k["ts"] + k["dur"]) for k in ks if short_name(k["name"]) in ("decode_kernel", "gather_rows_kernel")]
+    att = [(k["ts"], k["ts"] + k["dur"]) for k in ks if short_name(k["name"]).startswith("attn")]
+    overlap = {"attention_us": round(_measure(att), 2), "prefetch_us": round(_measure(pre), 2),
+               "both_us": round(_measure(_intersect(_union(pre), _union(att))), 2)}
+    overlap["attention_covered_frac"] = round(overlap["both_us"] / max(overlap["attention_us"], 1e-9), 4)
+    overlap["source"] = "CUPTI kernel activity (torch.profiler), one step of L layers"
     # prefetch alone (one layer, side stream idle otherwise)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(side_s):
@@ -934,6 +1003,9 @@ def run_offload(args, dist):
             "config": {"workload": f"c5: B={cfg.B} Hq={cfg.Hq} Hkv={cfg.Hkv} d={cfg.d} S={cfg.S} r={cfg.r} "
                                    f"k={cfg.k} {cfg.dtype}, K/V pools pinned host, {L} layers, q_hat cos 0.95"},
             "link_bytes_per_layer": link_bytes, "link_gbs": round(link_bytes / (us_layer * 1e-6) / 1e9, 2),
+            "link_peak": link,
+            "link_frac_of_h2d_peak": round(link_bytes / (us_layer * 1e-6) / 1e9 / link["h2d_gbs"], 4),
+            "overlap": overlap, "layers": L,
             "prefetch_alone_us": round(us_pf, 2),
             "prefetch_alone_link_gbs": round(link_bytes / (us_pf * 1e-6) / 1e9, 2),
             "jaccard_qhat_vs_q_mean": round(float(np.mean(jac)), 4),
