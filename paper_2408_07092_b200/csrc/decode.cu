@@ -701,8 +701,20 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     named_sync(kBarRegs, kThreads);  // the attention warps hold their registers
     pdl_trigger();
     const int stid = tid - kAttThreads, sw = warp - kAttWarps;
-    auto for_each_cand = [&](auto &&f) {  // (key, global token) with digit1 == D1, this CTA
-      if (!ovf) {
+    // Cluster-local tail (uniform over the cluster): when the cluster's D1
+    // tokens fit one list, every CTA copies all of them (one exchange, one
+    // pass of DSMEM reads) into h1 -- free once every CTA is past D1 -- and
+    // finishes the selection on its own, marking its own tokens: no further
+    // exchanges.  Otherwise the CTAs exchange histograms and members.
+    const bool loc = CL && tail && sh.state[2] <= (uint32_t)kCandCap;
+    uint2 *const gcand = loc ? reinterpret_cast<uint2 *>(sh.h1) : sh.cand;
+    static_assert(sizeof(sh.h1) >= kCandCap * sizeof(uint2), "cluster candidate buffer");
+    const int nchx = loc ? 1 : nch;  // CTAs whose histograms / members are combined
+    auto for_each_cand = [&](auto &&f) {  // (key, global token) with digit1 == D1: this CTA's, or the cluster's
+      if (loc) {
+        const int nc = (int)sh.state[2];
+        for (int i = stid; i < nc; i += kSelThreads) f(gcand[i].x, (int)gcand[i].y);
+      } else if (!ovf) {
         const int nc = (int)sh.ncand;
         for (int i = stid; i < nc; i += kSelThreads) f(sh.cand[i].x, (int)sh.cand[i].y);
       } else {  // more D1 tokens than the list holds: scan the keys
@@ -712,7 +724,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         }
       }
     };
-    auto mark = [&](int t) { atomicOr(&sh.selm[(t - t0) >> 5], 1u << ((t - t0) & 31)); };
+    auto mine = [&](int t) { return t >= t0 && t < t0 + nloc; };
+    auto mark = [&](int t) {
+      if (mine(t)) atomicOr(&sh.selm[(t - t0) >> 5], 1u << ((t - t0) & 31));
+    };
     auto sel_sync = [&] { named_sync(kBarSel, kSelThreads); };
     // cluster exchange point x: publish this CTA's data, wait for every CTA's
     auto exchange = [&](int x) {
@@ -724,18 +739,25 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       }
       DS_TRACE_BY(0, 2 * x + 1, kAttThreads);
     };
-    // boundary of a cluster 1024-bin histogram (32 coarse sums of 32 per CTA)
+    // sum of a word over the CTAs whose data is combined (just the local one
+    // in the cluster-local mode)
+    auto csum = [&](int n, const uint32_t *p) {
+      return loc ? (n > 0 ? *p : 0u) : cluster_sum(n, [&](int cr) { return *remote(p, cr); });
+    };
+    // boundary of a 1024-bin histogram (32 coarse sums of 32 per CTA), over
+    // the cluster or (local mode) this CTA alone
     auto boundary1024 = [&](uint32_t *hh, uint32_t *cc, uint32_t need, uint32_t *st, int x) {
       uint32_t v = hh[2 * stid] + hh[2 * stid + 1];
 #pragma unroll
       for (int o = 1; o < 16; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if ((stid & 15) == 0) cc[stid >> 4] = v;
-      exchange(x);
+      if (loc) sel_sync();
+      else exchange(x);
       if (sw == 0) {
         uint32_t w[1];
-        w[0] = cluster_sum(nch, [&](int cr) { return remote(cc, cr)[31 - lane]; });
+        w[0] = csum(nchx, cc + 31 - lane);
         const Boundary<1> cb = warp_boundary<1>(w, 31, 0u, need);
-        w[0] = cluster_sum(nch, [&](int cr) { return remote(hh, cr)[cb.bin * 32 + 31 - lane]; });
+        w[0] = csum(nchx, hh + cb.bin * 32 + 31 - lane);
         const Boundary<1> fb = warp_boundary<1>(w, cb.bin * 32 + 31, cb.above, need);
         if (lane == 0) {
           st[0] = (uint32_t)fb.bin;
@@ -747,6 +769,32 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       sel_sync();
       DS_TRACE_BY(0, 11 + x, kAttThreads);
     };
+    if (loc) {
+      // every CTA's candidate list is complete and every CTA is past D1
+      // (h1 is no longer read remotely): copy the cluster's candidates
+      exchange(0);
+      if (sw == 0) {
+        const uint32_t m = lane < nch ? remote(&sh.ncand, lane)[0] : 0u;
+        uint32_t incl = m;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        sh.c2[lane] = incl - m;  // exclusive offset of CTA lane's candidates
+      }
+      for (int i = stid; i < kD2; i += kSelThreads) sh.h2[i] = 0;  // (rebuilt over the cluster's candidates)
+      sel_sync();
+      const int nc = (int)sh.state[2];
+      for (int i = stid; i < nc; i += kSelThreads) {
+        int cr = 0;
+        for (int j = 1; j < nch; ++j) cr += (uint32_t)i >= sh.c2[j] ? 1 : 0;
+        const uint2 e = remote(sh.cand, cr)[i - (int)sh.c2[cr]];
+        gcand[i] = e;
+        atomicAdd(&sh.h2[(e.x >> kSh2) & (kD2 - 1)], 1u);
+      }
+      sel_sync();
+    }
     if (tail) {
       boundary1024(sh.h2, sh.c2, need1, sh.state + 3, 0);
       DS_TRACE_BY(1, 14, kAttThreads);
@@ -762,50 +810,58 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       });
       DS_TRACE_BY(0, 14, kAttThreads);
       if (!whole2 && fits2) {
-        exchange(1);  // every CTA's members are listed
-        // the cluster's members land in h2 (no CTA reads it after exchange 1)
-        uint2 *gathered = reinterpret_cast<uint2 *>(sh.h2);
-        static_assert(sizeof(sh.h2) >= kMaxMembers * sizeof(uint2), "member buffer");
-        // every CTA's member count in one round trip (lane cr of warp 0), the
-        // offsets in c2 (free after exchange 1), then every CTA's members in
-        // one pass so the remote reads of all CTAs overlap
-        if (sw == 0) {
-          const uint32_t m = lane < nch ? remote(&sh.nmem, lane)[0] : 0u;
-          uint32_t incl = m;
+        const uint2 *gathered = sh.members;  // (local mode: the cluster's members are all here)
+        if (!loc) {
+          exchange(1);  // every CTA's members are listed
+          // the cluster's members land in h2 (no CTA reads it after exchange 1)
+          uint2 *gm = reinterpret_cast<uint2 *>(sh.h2);
+          static_assert(sizeof(sh.h2) >= kMaxMembers * sizeof(uint2), "member buffer");
+          // every CTA's member count in one round trip (lane cr of warp 0), the
+          // offsets in c2 (free after exchange 1), then every CTA's members in
+          // one pass so the remote reads of all CTAs overlap
+          if (sw == 0) {
+            const uint32_t m = lane < nch ? remote(&sh.nmem, lane)[0] : 0u;
+            uint32_t incl = m;
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += y;
+            }
+            sh.c2[lane] = incl - m;  // exclusive offset of CTA lane
           }
-          sh.c2[lane] = incl - m;  // exclusive offset of CTA lane
-        }
-        sel_sync();
-        for (int i = stid; i < (int)cnt2; i += kSelThreads) {
-          int cr = 0;
-          for (int j = 1; j < nch; ++j) cr += (uint32_t)i >= sh.c2[j] ? 1 : 0;
-          gathered[i] = remote(sh.members, cr)[i - (int)sh.c2[cr]];
+          sel_sync();
+          for (int i = stid; i < (int)cnt2; i += kSelThreads) {
+            int cr = 0;
+            for (int j = 1; j < nch; ++j) cr += (uint32_t)i >= sh.c2[j] ? 1 : 0;
+            gm[i] = remote(sh.members, cr)[i - (int)sh.c2[cr]];
+          }
+          gathered = gm;
         }
         sel_sync();
         DS_TRACE_BY(1, 15, kAttThreads);
         const int nm = (int)cnt2;  // rank by (key desc, token asc)
         for (int i = stid; i < nm; i += kSelThreads) {
           const uint2 me = gathered[i];
+          if (!mine((int)me.y)) continue;
           uint32_t rank = 0;
           for (int j = 0; j < nm; ++j) {
             const uint2 o = gathered[j];
             rank += (o.x > me.x) || (o.x == me.x && o.y < me.y);
           }
-          if (rank < need2 && (int)me.y >= t0 && (int)me.y < t0 + nloc) mark((int)me.y);
+          if (rank < need2) mark((int)me.y);
         }
       } else if (!whole2) {
         // massive ties at the 22-bit prefix: digit 3, then token order among
-        // the keys equal to kB (h1 / c1 and eqm are no longer read by anyone)
-        uint32_t *h3 = sh.h1, *c3 = sh.c1;
+        // the keys equal to kB (h1 / c1 and eqm are no longer read by anyone;
+        // local mode: h1 holds the candidates, members are unused here)
+        uint32_t *h3 = loc ? reinterpret_cast<uint32_t *>(sh.members) : sh.h1, *c3 = sh.c1;
+        static_assert(sizeof(sh.members) >= kD3 * sizeof(uint32_t), "digit-3 histogram");
         for (int i = stid; i < kD3; i += kSelThreads) h3[i] = 0;
         for (int g = stid; g < ngrp; g += kSelThreads) sh.eqm[g] = 0;
+        if (stid == 0) sh.lower_sel = sh.cnt[1] = 0;
         sel_sync();
         for_each_cand([&](uint32_t key, int t) {
-          if ((key >> kSh2) == P2) atomicAdd(&h3[key & (kD3 - 1)], 1u);
+          if ((key >> kSh2) == P2 && (loc || mine(t))) atomicAdd(&h3[key & (kD3 - 1)], 1u);
         });
         sel_sync();
         boundary1024(h3, c3, need2, sh.state + 6, 2);
@@ -813,11 +869,25 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         const uint32_t rem = need2 - sh.state[7];  // keys == kB taken, lowest tokens first
         for_each_cand([&](uint32_t key, int t) {
           if ((key >> kSh2) == P2 && key > kB) mark(t);
-          else if (key == kB) atomicOr(&sh.eqm[(t - t0) >> 5], 1u << ((t - t0) & 31));
+          else if (key == kB) {
+            if (mine(t)) {
+              atomicOr(&sh.eqm[(t - t0) >> 5], 1u << ((t - t0) & 31));
+              if (loc) atomicAdd(&sh.cnt[1], 1u);
+            } else if (t < t0) {
+              atomicAdd(&sh.lower_sel, 1u);  // (local mode: a lower CTA's key == kB)
+            }
+          }
         });
+        sel_sync();
         // keys == kB in lower CTAs (h3 is final on every CTA after exchange 2)
-        const uint32_t eq_lower = cluster_sum(crank, [&](int cr) { return remote(h3, cr)[kB & (kD3 - 1)]; });
-        const uint32_t my_eq = h3[kB & (kD3 - 1)];
+        uint32_t eq_lower = 0u, my_eq = 0u;
+        if (loc) {
+          eq_lower = sh.lower_sel;
+          my_eq = sh.cnt[1];
+        } else {
+          eq_lower = cluster_sum(crank, [&](int cr) { return remote(h3, cr)[kB & (kD3 - 1)]; });
+          my_eq = h3[kB & (kD3 - 1)];
+        }
         const uint32_t take = rem > eq_lower ? min(rem - eq_lower, my_eq) : 0u;
         sel_sync();
         if (sw == 0 && take > 0) {  // the take-th local key == kB, token order

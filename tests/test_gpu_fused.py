@@ -99,12 +99,22 @@ def test_fused_all_tied_takes_lowest_indices():
             check_output(y[b, h * 4 + g].float().cpu().numpy(), ref, "bf16")
 
 
+TIE_CFGS = {
+    "one_cta": (synth.Config("fd", B=16, Hq=32, Hkv=8, d=128, S=5000, r=8, k=600, dtype="bf16"), 600),
+    # 8 units -> clusters of 8 CTAs: the cluster-local tail (the D1 bin fits
+    # one list) with members / digit-3 ties, and the exchange tail ("narrow")
+    "cluster9k": (synth.Config("fc", B=2, Hq=16, Hkv=4, d=128, S=9000, r=8, k=1080, dtype="bf16"), 1080),
+    "cluster12k": (synth.Config("fe", B=2, Hq=16, Hkv=4, d=128, S=12000, r=8, k=1440, dtype="bf16"), 1440),
+}
+
+
+@pytest.mark.parametrize("geom", list(TIE_CFGS))
 @pytest.mark.parametrize("span", ["duplicates", "narrow"])
-def test_fused_duplicate_and_narrow_scores(span):
+def test_fused_duplicate_and_narrow_scores(span, geom):
     """Label values from a tiny set: many exactly equal scores at the
     boundary ("duplicates": members + ties) and, for "narrow", all scores in
     one 12-bit digit so the candidate list overflows (key-scan path)."""
-    cfg = synth.Config("fd", B=16, Hq=32, Hkv=8, d=128, S=5000, r=8, k=600, dtype="bf16")
+    cfg, k = TIE_CFGS[geom]
     lay, cache, C = build_cache(cfg)
     g = torch.Generator(device="cuda").manual_seed(3)
     if span == "duplicates":
@@ -118,15 +128,16 @@ def test_fused_duplicate_and_narrow_scores(span):
     ds.prefill(cache, lay.K, lay.V, lay.seq_lens)
     lay.q.zero_()
     for h in range(cfg.Hkv):  # q_lab = 1 on every channel (head 0 of the group carries it)
-        lay.q[:, h * 4, C[h].long().cuda()] = 1.0
-    y, idx = run(cache, lay, 600)
-    for b, h in [(0, 0), (9, 5), (15, 7)]:
+        lay.q[:, h * cfg.G, C[h].long().cuda()] = 1.0
+    y, idx = run(cache, lay, k)
+    units = [(0, 0), (9, 5), (15, 7)] if cfg.B == 16 else [(0, 0), (1, 3), (1, 1)]
+    for b, h in units:
         q, K, V = unit_host(lay, b, h)
         L = oracle.label_gather(K, C[h].numpy())
-        yr, idx_ref, _, _ = oracle.ds_decode_unit(q, K, V, L, C[h].numpy(), 600)
+        yr, idx_ref, _, _ = oracle.ds_decode_unit(q, K, V, L, C[h].numpy(), k)
         assert idx[b, h].cpu().numpy().tolist() == idx_ref.tolist()
-        for gq in range(4):
-            check_output(y[b, h * 4 + gq].float().cpu().numpy(), yr[gq], "bf16")
+        for gq in range(cfg.G):
+            check_output(y[b, h * cfg.G + gq].float().cpu().numpy(), yr[gq], "bf16")
 
 
 def test_fused_full_density_equals_dense():
