@@ -227,6 +227,27 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&sh.xbar[i])), "r"(nch) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  {
+    // The label rows of this CTA's chunk (and its block-table slice) go to L2
+    // before the wait: the preceding kernel does not produce them (it may
+    // write one new row, which the L2 keeps coherent; they are read into
+    // registers only after the wait), so their HBM reads overlap its drain.
+    const int t0p = crank * p.chunk, mloc = max(0, min(p.chunk, c.Smax - t0p));
+    const size_t lr0 = ((size_t)b * c.Hkv + h) * (size_t)c.Smax + t0p;
+    if (!p.l2_prefetch) {
+    } else if (tid == 0 && !lnone) {
+      if (!lq4) {
+        prefetch_l2((const T *)c.label + lr0 * (size_t)c.r, (size_t)mloc * c.r * sizeof(T));
+      } else if (((lr0 * c.rb) & 15) == 0 && ((lr0 * sizeof(T)) & 15) == 0) {
+        prefetch_l2((const uint8_t *)c.label + lr0 * c.rb, (size_t)mloc * c.rb);
+        prefetch_l2((const T *)c.label_scale + lr0, (size_t)mloc * sizeof(T));
+      }
+    } else if (tid == 32) {
+      const int pg0 = t0p / c.P, npg = (mloc + c.P - 1) / c.P + 1;
+      const int32_t *btp = c.block_table + (size_t)b * c.maxp + pg0;
+      if (((uintptr_t)btp & 15) == 0) prefetch_l2(btp, (size_t)min(npg, c.maxp - pg0) * 4 & ~(size_t)15);
+    }
+  }
   pdl_wait();  // label / KV rows may come from the preceding append
   // (dependents are released only after the register split below: a CTA of
   // the next kernel must not take the registers the selection warps free)
@@ -1522,6 +1543,17 @@ cudaError_t launch_fused(const ds_cache *c, FusedParams p, cudaStream_t st) {
   const int chunk = fused_chunk(c, nch);
   if (chunk > kMaxS) return cudaErrorInvalidValue;
   p.chunk = chunk;
+  {
+    // label L2 prefetch before the PDL wait: measured to help when CTAs start
+    // in several waves (c4: 512 units) or as clusters (c5), and to cost
+    // ~1 us when every unit has one CTA of a single wave (c3: the burst
+    // delays the first demand loads)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long units = (long)c->batch * (c->group_reduce == DS_GROUP_PER_HEAD ? c->num_q_heads : c->num_kv_heads);
+    p.l2_prefetch = nch > 1 || units * nch > sms;
+  }
 #define DS_F(T)                                                                                         \
   if (c->head_dim == 64) return c->r == 8 ? launch_t<T, 8, 64>(c, p, nch, st) : launch_t<T, 0, 64>(c, p, nch, st); \
   return c->r == 8 ? launch_t<T, 8, 128>(c, p, nch, st) : launch_t<T, 0, 128>(c, p, nch, st);

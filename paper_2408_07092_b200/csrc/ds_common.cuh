@@ -122,6 +122,17 @@ template <> __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi
 // dependents after that wait, so any pre-wait read is of data written two or
 // more launches earlier (complete by then).  Both are no-ops without PDL.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// L2 prefetch of [p, p + bytes) (bulk, asynchronous, no data returned to the
+// SM): safe before pdl_wait() even for data the predecessor may still write,
+// since the L2 stays coherent and nothing is read into registers.  p and
+// bytes are 16-B multiples.
+__device__ __forceinline__ void prefetch_l2(const void *p, size_t bytes) {
+  const char *a = static_cast<const char *>(p);
+  for (size_t off = 0; off < bytes; off += 65536) {
+    const uint32_t n = (uint32_t)(bytes - off < 65536 ? bytes - off : 65536) & ~15u;
+    if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a + off), "r"(n) : "memory");
+  }
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 // ------------------------------------------------------------- misc

@@ -59,6 +59,9 @@ struct FusedParams {
   // positions[b], k_new / v_new [B][1][Hkv][D]; nullptr = no append
   const void *k_new, *v_new;
   const int32_t *positions;
+  // L2 prefetch of each CTA's label rows before griddepcontrol.wait (set by
+  // launch_fused when the grid has more CTAs than SMs or clusters)
+  int l2_prefetch;
 };
 constexpr int kFusedMaxSmem = 227 * 1024;
 bool fused_applicable(const ds_cache *c);
