@@ -860,42 +860,15 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         }
         sel_sync();
         DS_TRACE_BY(1, 15, kAttThreads);
-        // rank by (key desc, token asc).  The members share the 22-bit
-        // prefix, so the number of larger keys is a suffix sum of their
-        // digit-3 histogram (a counting sort); only keys shared by several
-        // members compare tokens.  (h2 / h1 are free here.)
-        const int nm = (int)cnt2;
-        uint32_t *h3 = loc ? sh.h2 : sh.h1;
-        static_assert(kD3 == 2 * kSelThreads, "two digit-3 bins per selection thread");
-        h3[2 * stid] = h3[2 * stid + 1] = 0u;
-        sel_sync();
-        for (int i = stid; i < nm; i += kSelThreads) atomicAdd(&h3[gathered[i].x & (kD3 - 1)], 1u);
-        sel_sync();
-        {  // in place: h3[d] = number of members with digit 3 above d (bins taken high to low)
-          const int hi = kD3 - 1 - 2 * stid;
-          const uint32_t a = h3[hi], bq = h3[hi - 1], tot = a + bq;
-          uint32_t incl = tot;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-          }
-          if (lane == 31) sh.wtot[kAttWarps + sw] = incl;
-          sel_sync();
-          uint32_t ex = incl - tot;
-          for (int w = 0; w < sw; ++w) ex += sh.wtot[kAttWarps + w];
-          h3[hi] = ex;
-          h3[hi - 1] = ex + a;
-        }
-        sel_sync();
+        const int nm = (int)cnt2;  // rank by (key desc, token asc)
         for (int i = stid; i < nm; i += kSelThreads) {
           const uint2 me = gathered[i];
           if (!mine((int)me.y)) continue;
-          const uint32_t d = me.x & (kD3 - 1);
-          uint32_t rank = h3[d];
-          const uint32_t same = (d == 0 ? (uint32_t)nm : h3[d - 1]) - rank;  // members with this key
-          if (same > 1)
-            for (int j = 0; j < nm; ++j) rank += gathered[j].x == me.x && gathered[j].y < me.y;
+          uint32_t rank = 0;
+          for (int j = 0; j < nm; ++j) {
+            const uint2 o = gathered[j];
+            rank += (o.x > me.x) || (o.x == me.x && o.y < me.y);
+          }
           if (rank < need2) mark((int)me.y);
         }
       } else if (!whole2) {
