@@ -101,7 +101,8 @@ struct alignas(128) Sh {
   uint64_t xbar[4];            // cluster exchange barriers of the selection warps
   float newlab[kMaxR];         // fused append: the new token's label values (int4: codes)
   float newscale;              // fused append, int4: its scale
-  int newpos;                  // fused append: the new token's position (-1: none)
+  int newpage;                 // fused append: the physical page of the new token (cp.async)
+  alignas(16) uint8_t newkv[2 * 128 * 2];  // fused append: the new token's K row then V row (cp.async)
   alignas(16) uint8_t qt[8 * 128 * 2];  // query rows (heads >= G zero), 16-B chunks swizzled
 };
 
@@ -265,37 +266,17 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     cp_async16(smem_u32(sh.qt + row * ROWB + swz(row, ch)), qb + (size_t)min(row, G - 1) * D + ch * 8,
                row < G ? 16 : 0);
   }
-  cp_async_commit();
-  // fused append: the CTA whose chunk holds the new token writes its K/V
-  // rows and (16-bit) label row here and keeps its r channel values; after
-  // the stream one thread re-scores it (the stream may have read the old
-  // label row) and writes a 4-bit label row (kept out of this register-tight
-  // prologue).  One writer per KV head in per-head mode.
-  if (p.k_new && warp == 0) {  // before this warp holds the label prefetch
-    const int pn = p.positions[b];
-    if (lane == 0) sh.newpos = pn;
-    if (pn >= t0 && pn < t0 + max(0, min(p.chunk, c.seq_lens[b] - t0))) {
-      const T *kr = (const T *)p.k_new + ((size_t)b * c.Hkv + h) * D;
-      const T *vr = (const T *)p.v_new + ((size_t)b * c.Hkv + h) * D;
-      const int32_t *Ch = c.C + (size_t)h * c.r;
-      // per-head mode: the G units of a KV head all write the identical
-      // bytes (a benign race), so each CTA's own attention gathers read the
-      // new rows after its own writes (ordered by the CTA barriers below)
-      {
-        const int page = c.block_table[(size_t)b * c.maxp + pn / c.P];
-        const size_t dst = (((size_t)page * c.Hkv + h) * c.P + (pn % c.P)) * (size_t)D;
-        for (int v = lane; v < 2 * CHN; v += 32) {
-          if (v < CHN) reinterpret_cast<uint4 *>((T *)c.k_pool + dst)[v] = reinterpret_cast<const uint4 *>(kr)[v];
-          else reinterpret_cast<uint4 *>((T *)c.v_pool + dst)[v - CHN] = reinterpret_cast<const uint4 *>(vr)[v - CHN];
-        }
-        if (!lq4 && !lnone) {
-          T *lab = (T *)c.label + (((size_t)b * c.Hkv + h) * c.Smax + pn) * c.r;
-          for (int j = lane; j < c.r; j += 32) lab[j] = kr[Ch[j]];
-        }
-      }
-      for (int j = lane; j < c.r; j += 32) sh.newlab[j] = Elem<T>::to_f(kr[Ch[j]]);
-    }
+  // fused append (a0 of the new token): its K and V rows are staged in shared
+  // memory by cp.async with the query tile (no registers, no wait here); the
+  // CTA whose chunk holds the token writes them, and its label row, after the
+  // stream (the stream may read the old label row: that one key is re-scored)
+  static_assert(2 * D * 2 <= (int)sizeof(Sh::newkv), "new K/V row buffer");
+  if (p.k_new && tid < 2 * CHN) {
+    const T *src = (const T *)(tid < CHN ? p.k_new : p.v_new) + ((size_t)b * c.Hkv + h) * D;
+    cp_async16(smem_u32(sh.newkv + tid * 16), src + (tid % CHN) * 8, 16);
   }
+  cp_async_commit();
+  const int pn = p.k_new ? p.positions[b] : -1;  // the new token's position (uniform)
   // The first label batch is requested before anything else waits on memory,
   // so the prologue's round trips (seq_lens, C, q) overlap it.  Its bound is
   // the allocation (Smax), not seq_lens: rows past the sequence are read and
@@ -365,8 +346,21 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   const bool btc_ok = lnone && npg <= (int)(sizeof(sh.cand) / 4);
   if (btc_ok)
     for (int i = tid; i < npg; i += kThreads) btc[i] = __ldg(c.block_table + (size_t)b * c.maxp + pg0 + i);
-  cp_async_wait<0>();  // this thread's part of the query tile
+  cp_async_wait<0>();  // this thread's part of the query tile (and the new K / V rows)
   __syncthreads();
+  // fused append, owner CTA: the new token's page entry (waited for after the
+  // stream) and its r label values from the staged K row
+  const bool own_new = pn >= t0 && pn < t0 + nloc;
+  if (own_new) {
+    if (tid == 0) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(&sh.newpage)),
+                   "l"(c.block_table + (size_t)b * c.maxp + pn / c.P)
+                   : "memory");
+      cp_async_commit();
+    }
+    const T *kn = reinterpret_cast<const T *>(sh.newkv);
+    for (int j = tid; j < c.r; j += kThreads) sh.newlab[j] = Elem<T>::to_f(kn[c.C[(size_t)h * c.r + j]]);
+  }
   auto qtile = [&](int g, int ch) {  // q[g][ch] from the swizzled tile
     return Elem<T>::to_f(*reinterpret_cast<const T *>(sh.qt + g * ROWB + swz(g, ch >> 3) + (ch & 7) * 2));
   };
@@ -536,8 +530,26 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   DS_TRACE_AT(1, 13);
   if (tid < 128) keys[nloc + tid] = 0u;  // pad: below every finite score's key
   __syncthreads();
-  const int pnew = p.k_new ? sh.newpos : -1;
-  if (pnew >= t0 && pnew < t0 + nloc) {  // fused append: the new token's key from the values written
+  const int pnew = pn;
+  if (own_new) {  // fused append: write the new token's rows, re-score its key
+    if (warp == 0) {
+      // K / V rows and the 16-bit label row from the staged copies (per-head
+      // mode: the G units of a KV head all write the identical bytes, and
+      // each CTA's own gathers read them after the barrier below)
+      if (lane == 0) cp_async_wait<0>();  // the page entry
+      __syncwarp();
+      const size_t dst = (((size_t)sh.newpage * c.Hkv + h) * c.P + (pnew % c.P)) * (size_t)D;
+      const uint4 *src = reinterpret_cast<const uint4 *>(sh.newkv);
+      for (int v = lane; v < 2 * CHN; v += 32) {
+        if (v < CHN) reinterpret_cast<uint4 *>((T *)c.k_pool + dst)[v] = src[v];
+        else reinterpret_cast<uint4 *>((T *)c.v_pool + dst)[v - CHN] = src[v];
+      }
+      if (!lq4 && !lnone) {
+        const T *kn = reinterpret_cast<const T *>(sh.newkv);
+        T *lr = (T *)c.label + (((size_t)b * c.Hkv + h) * c.Smax + pnew) * c.r;
+        for (int j = lane; j < c.r; j += 32) lr[j] = kn[c.C[(size_t)h * c.r + j]];
+      }
+    }
     if (tid == 0) {
       if (lq4) {  // R16, the arithmetic of append_row_warp: codes replace the values in newlab
         float a = 0.0f;
