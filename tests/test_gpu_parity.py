@@ -226,3 +226,15 @@ def test_full_size_sampled_units(name):
     assert (iv[..., 1:] > iv[..., :-1]).all() and (iv >= 0).all() and (iv < cfg.S).all()
     del cache, lay
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("S,k", [(300000, 18750), (40000, 2500)])
+def test_long_sequence_large_cluster(S, k):
+    """S beyond 8 x 32K keys: a non-portable cluster of ceil(S / 32K) CTAs
+    per unit (10 at S = 300K, after the occupancy check), and a ragged
+    second sequence; every unit against the oracle."""
+    cfg = synth.Config("ls", B=2, Hq=4, Hkv=1, d=128, S=S, r=8, k=k, dtype="bf16")
+    lay, cache, C = build_cache(cfg, seq_lens=[S, S - 4321])
+    assert ds.ds_decode_launches(cache, k) == 1, "expected the single-kernel cluster path"
+    y, idx = run_decode(cache, lay, k)
+    check_units(lay, cache, C, k, all_units(cfg), y, idx)
