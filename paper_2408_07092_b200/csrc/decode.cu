@@ -112,7 +112,11 @@ struct Geo {
   static constexpr int CHN = ROWB / 16;                 // 16-B chunks per row
   static constexpr int STAGE = 2 * kBatch * ROWB;       // K rows then V rows of a batch
   static constexpr int RING = kAttWarps * 2 * STAGE;    // 2 stages per attention warp
-  static constexpr int PART = (2 * kAttWarps * 8 + kAttWarps * 8 * D) * 4;  // warp partials
+  // warp partials: m, l per head, O rows with a stride of D + 4 floats, so
+  // the fragment stores of one warp (heads 2tq, 2tq + 1; columns gq) hit 32
+  // distinct banks
+  static constexpr int WOS = D + 4;
+  static constexpr int PART = (2 * kAttWarps * 8 + kAttWarps * 8 * WOS) * 4;
   static constexpr int CPART = (16 + 8 * D + 8 * kAttWarps) * 4;          // then the CTA partial + weights
   static_assert(CHN >= 8, "row swizzle needs >= 8 chunks");
 };
@@ -1310,19 +1314,26 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
     float *wm = reinterpret_cast<float *>(region);  // [16][8]
     float *wl = wm + kAttWarps * 8;                 // [16][8]
-    float *wo = wl + kAttWarps * 8;                 // [16][8][D]
+    float *wo = wl + kAttWarps * 8;                 // [16][8][WOS]
+    constexpr int WOS = GE::WOS;
     named_sync(kBarAtt, kAttThreads);               // ring no longer read
     if (tq == 0) {
       wm[aw * 8 + gq] = m_run;
       wl[aw * 8 + gq] = l_run;
     }
+    // (only the G real heads: rows >= G of the tile are padding)
+    const bool h0ok = 2 * tq < G, h1ok = 2 * tq + 1 < G;
 #pragma unroll
     for (int mt = 0; mt < NKS; ++mt) {
-      float *w0 = wo + (size_t)(aw * 8 + 2 * tq) * D + 16 * mt + gq;
-      w0[0] = o[mt][0];
-      w0[D] = o[mt][1];
-      w0[8] = o[mt][2];
-      w0[D + 8] = o[mt][3];
+      float *w0 = wo + (size_t)(aw * 8 + 2 * tq) * WOS + 16 * mt + gq;
+      if (h0ok) {
+        w0[0] = o[mt][0];
+        w0[8] = o[mt][2];
+      }
+      if (h1ok) {
+        w0[WOS] = o[mt][1];
+        w0[WOS + 8] = o[mt][3];
+      }
     }
     named_sync(kBarAtt, kAttThreads);
     DS_TRACE_AT(1, 10);
@@ -1341,7 +1352,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         for (int w = 0; w < kAttWarps; ++w) {
           const float e = exp2f(wm[w * 8 + g] - M);  // 0 for a warp without rows (m = -inf)
           L = fmaf(wl[w * 8 + g], e, L);
-          O = fmaf(wo[(size_t)(w * 8 + g) * D + dd], e, O);
+          O = fmaf(wo[(size_t)(w * 8 + g) * WOS + dd], e, O);
         }
         outp[i] = Elem<T>::from_f(O / L);
       }
@@ -1371,7 +1382,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         const int g = i / D, dd = i - (i / D) * D;
         float O = 0.f;
 #pragma unroll
-        for (int w = 0; w < kAttWarps; ++w) O = fmaf(wo[(size_t)(w * 8 + g) * D + dd], wsc[g * kAttWarps + w], O);
+        for (int w = 0; w < kAttWarps; ++w) O = fmaf(wo[(size_t)(w * 8 + g) * WOS + dd], wsc[g * kAttWarps + w], O);
         cm[16 + i] = O;
       }
       cluster_sync_warp(true);  // every CTA's partial is complete
