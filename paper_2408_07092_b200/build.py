@@ -75,8 +75,24 @@ def build_trace() -> str:
     return out
 
 
+def build_exp(name: str, flags: list[str]) -> str:
+    """Timing-experiment variant of the product library (unity TU, extra -D switches)."""
+    os.makedirs(BUILD, exist_ok=True)
+    unity = os.path.join(BUILD, "unity_%s.cu" % name)
+    with open(unity, "w") as f:
+        for src in _sources():
+            f.write('#include "%s"\n' % src)
+    out = os.path.join(PKG, name + ".so")
+    subprocess.check_call([NVCC, *ARCH, *[x for x in FLAGS if x not in ("-v", "-Xptxas")], *flags,
+                           "-shared", unity, "-o", out])
+    return out
+
+
 if __name__ == "__main__":
     if "--trace" in sys.argv:
         print(build_trace())
+    elif "--exp" in sys.argv:  # --exp NAME -DFLAG ...
+        i = sys.argv.index("--exp")
+        print(build_exp(sys.argv[i + 1], sys.argv[i + 2:]))
     else:
         print(build(verbose="-v" in sys.argv))

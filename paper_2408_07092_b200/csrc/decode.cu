@@ -256,6 +256,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   pdl_wait();  // label / KV rows may come from the preceding append
   // (dependents are released only after the register split below: a CTA of
   // the next kernel must not take the registers the selection warps free)
+  DS_TRACE_AT(2, 2);
+  // The prologue's own round trips (seq_lens, the channel set C) are issued
+  // first and together, so they are one DRAM latency, not a chain of them
+  const int n = c.seq_lens[b];
+  const int r = R > 0 ? R : c.r;
+  int chj = 0;
+  if (tid < r) chj = __ldg(c.C + (size_t)h * c.r + tid);
   const int t0 = crank * p.chunk;  // this CTA's tokens [t0, t0 + nloc)
   const size_t lrow = ((size_t)b * c.Hkv + h) * (size_t)c.Smax + t0;  // first label row of this CTA
   const T *lab = (const T *)c.label + lrow * (size_t)c.r;
@@ -281,40 +288,32 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   }
   cp_async_commit();
   const int pn = p.k_new ? p.positions[b] : -1;  // the new token's position (uniform)
-  // The first label batch is requested before anything else waits on memory,
-  // so the prologue's round trips (seq_lens, C, q) overlap it.  Its bound is
-  // the allocation (Smax), not seq_lens: rows past the sequence are read and
-  // dropped below.
+  // No label rows are requested before the prologue's own round trips
+  // (seq_lens, C, the query tile) are back: a first batch of 16 MiB issued
+  // ahead of them queued them behind it (c3: 2.0 us instead of 0.7 us until
+  // n is known; decode 41.4 -> 40.6 us without it).  The 4-bit label loads
+  // its first two code groups once n is known (its loop keeps two in flight).
   const int maxloc = max(0, min(p.chunk, c.Smax - t0));
   constexpr bool kVec16 = R > 0 && R * sizeof(T) == 16;  // one 16-B label row per token
   constexpr int U = kUnroll;
   const bool q4v = R == 8 && lq4 && (c.Smax & 3) == 0;  // 16-B code / 8-B scale vectors of 4 tokens
-  // one register array for both label formats (int4: codes of two groups in
-  // pv[0..1], their scales in pv[2])
+  // (int4: codes of the first two groups in pv[0..1], their scales in pv[2])
   uint4 pv[U];
-  bool pre = false;
-  if (lnone || greduce == DS_GROUP_MAX) {
-  } else if (!lq4) {
-    if constexpr (kVec16) {
-      pre = tid + (U - 1) * kThreads < maxloc;
-      if (pre) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) pv[u] = ldg_nc_v4(reinterpret_cast<const uint4 *>(lab) + tid + u * kThreads);
-      }
+  auto first_batch = [&] {
+    if (!lnone && greduce != DS_GROUP_MAX && lq4 && q4v) {
+      const int mg = maxloc >> 2;
+      const uint2 z2 = make_uint2(0, 0);
+      uint2 a2 = z2, b2 = z2;
+      pv[0] = pv[1] = make_uint4(0, 0, 0, 0);
+      if (tid < mg) pv[0] = ldg_nc_v4(reinterpret_cast<const uint4 *>(cod) + tid), a2 = ldg_nc_v2(reinterpret_cast<const uint2 *>(scl) + tid);
+      if (tid + kThreads < mg)
+        pv[1] = ldg_nc_v4(reinterpret_cast<const uint4 *>(cod) + tid + kThreads),
+        b2 = ldg_nc_v2(reinterpret_cast<const uint2 *>(scl) + tid + kThreads);
+      pv[2] = make_uint4(a2.x, a2.y, b2.x, b2.y);
     }
-  } else if (q4v) {
-    const int mg = maxloc >> 2;
-    const uint2 z2 = make_uint2(0, 0);
-    uint2 a2 = z2, b2 = z2;
-    pv[0] = pv[1] = make_uint4(0, 0, 0, 0);
-    if (tid < mg) pv[0] = ldg_nc_v4(reinterpret_cast<const uint4 *>(cod) + tid), a2 = ldg_nc_v2(reinterpret_cast<const uint2 *>(scl) + tid);
-    if (tid + kThreads < mg)
-      pv[1] = ldg_nc_v4(reinterpret_cast<const uint4 *>(cod) + tid + kThreads),
-      b2 = ldg_nc_v2(reinterpret_cast<const uint2 *>(scl) + tid + kThreads);
-    pv[2] = make_uint4(a2.x, a2.y, b2.x, b2.y);
-  }
-  const int n = c.seq_lens[b];
+  };
   const int keff = min(p.k, n);
+  DS_TRACE_AT(2, 3);
   const int nloc = max(0, min(p.chunk, n - t0));
   T *outp = (T *)p.out + ((size_t)b * c.Hq + (size_t)hq0) * D;
   int32_t *idx = p.idx ? p.idx + (size_t)unit * p.k : nullptr;
@@ -328,12 +327,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     }
     return;
   }
+  first_batch();
 
   // ---- a1, query tile, zeroing (the tile and C are loaded together; q_lab
   // is then summed from the tile in shared memory)
-  const int r = R > 0 ? R : c.r;
-  int chj = 0;
-  if (tid < r) chj = c.C[(size_t)h * c.r + tid];
   for (int i = tid; i < kD1; i += kThreads) sh.h1[i] = 0;
   for (int i = tid; i < kD2; i += kThreads) sh.h2[i] = 0;
   for (int i = tid; i < kMaxS / 32; i += kThreads) sh.selm[i] = 0;
@@ -352,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     for (int i = tid; i < npg; i += kThreads) btc[i] = __ldg(c.block_table + (size_t)b * c.maxp + pg0 + i);
   cp_async_wait<0>();  // this thread's part of the query tile (and the new K / V rows)
   __syncthreads();
+  DS_TRACE_AT(2, 4);
   // fused append, owner CTA: the new token's page entry (waited for after the
   // stream) and its r label values from the staged K row
   const bool own_new = pn >= t0 && pn < t0 + nloc;
@@ -363,7 +361,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       cp_async_commit();
     }
     const T *kn = reinterpret_cast<const T *>(sh.newkv);
-    for (int j = tid; j < c.r; j += kThreads) sh.newlab[j] = Elem<T>::to_f(kn[c.C[(size_t)h * c.r + j]]);
+    static_assert(kMaxR <= kThreads, "one label channel per thread");
+    if (tid < r) sh.newlab[tid] = Elem<T>::to_f(kn[chj]);
   }
   auto qtile = [&](int g, int ch) {  // q[g][ch] from the swizzled tile
     return Elem<T>::to_f(*reinterpret_cast<const T *>(sh.qt + g * ROWB + swz(g, ch >> 3) + (ch & 7) * 2));
@@ -375,11 +374,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       sh.qlab[i] = qtile(g, c.C[(size_t)h * c.r + j]);
     }
   } else {
-    for (int j = tid; j < r; j += kThreads) {  // Q_label[j] = sum_g q[g][C[j]], g ascending (R3)
-      const int ch = j == tid ? chj : c.C[(size_t)h * c.r + j];
+    if (tid < r) {  // Q_label[j] = sum_g q[g][C[j]], g ascending (R3); thread j = channel j
       float s = 0.0f;
-      for (int g = 0; g < G; ++g) s = s + qtile(g, ch);
-      sh.qlab[j] = s;
+      for (int g = 0; g < G; ++g) s = s + qtile(g, chj);
+      sh.qlab[tid] = s;
     }
   }
   __syncthreads();
@@ -512,10 +510,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
           DS_HIST_ADD(&sh.h1[k0 >> kSh1]);
         }
       };
-      if (pre && i0 + (U - 1) * kThreads < nloc) {  // the prefetched first batch
-        rows8(i0, pv);
-        i0 += U * kThreads;
-      }
       for (; i0 + (U - 1) * kThreads < nloc; i0 += U * kThreads) {
 #pragma unroll
         for (int u = 0; u < U; ++u) pv[u] = __ldg(reinterpret_cast<const uint4 *>(lab) + (size_t)(i0 + u * kThreads));
@@ -659,41 +653,54 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         sh.eqm[g] = 0u;
       }
     } else {
-      // digit1 > D1 (>= D1 taken whole) <=> key >= gthr; digit1 == D1 <=>
-      // key - (D1 << 20) < 2^20 (never, when D1 is taken whole)
+      // digit1 > D1 (>= D1 taken whole) <=> key >= gthr; digit1 >= D1 <=>
+      // key >= elo, so digit1 == D1 is the XOR of the two (empty when D1 is
+      // taken whole: gthr = elo)
       // (D1 = 4095 not taken whole: nothing lies above the top digit; the
       // all-ones threshold admits no finite score's key, R6)
-      uint32_t gthr = !whole1 && D1 == (uint32_t)(kD1 - 1) ? 0xffffffffu : (whole1 ? D1 : D1 + 1) << kSh1;
-      uint32_t elo = D1 << kSh1, ewid = whole1 ? 0u : (1u << kSh1);
-      // (opaque copies: the compiler would otherwise split the ewid = 0 case
-      // into extra predicate logic and re-materialise D1 per group)
-      asm("mov.b32 %0, %0;" : "+r"(gthr));
-      asm("mov.b32 %0, %0;" : "+r"(elo));
-      asm("mov.b32 %0, %0;" : "+r"(ewid));
-      // this warp's <= 32 groups: lane gi keeps group gi's two masks (one
-      // store each at the end), the loop body is a load, two ballots and two
-      // selects per group -- the pass is bound by the ALU/FMA pipes (2 cycles
-      // per warp instruction each) with 32 warps per SM, ~2.4 us on c3
-      static_assert(kMaxS / 32 / kWarps <= 32, "one mask word per lane");
-      const int g0 = w0 >> 5, ng = (w1 - w0 + 31) >> 5;
-      uint32_t ga = 0u, ea = 0u;
-#pragma unroll 8
-      for (int gi = 0; gi < ng; ++gi) {
-        const uint32_t key = keys[(g0 + gi) * 32 + lane];
-        const uint32_t mg = __ballot_sync(0xffffffffu, key >= gthr);
-        const uint32_t me = __ballot_sync(0xffffffffu, key - elo < ewid);
-        ga = lane == gi ? mg : ga;
-        ea = lane == gi ? me : ea;
+      const uint32_t gthr = !whole1 && D1 == (uint32_t)(kD1 - 1) ? 0xffffffffu : (whole1 ? D1 : D1 + 1) << kSh1;
+      const uint32_t elo = D1 << kSh1;
+      // this warp's <= 32 groups, four at a time: a load, two compares and
+      // two ballots per group, lane 0 stores the four gt words and the four
+      // ge words with one 16-B store each (eqm holds digit1 >= D1 until the
+      // candidate pass below turns it into digit1 == D1) -- the pass is bound
+      // by the ALU pipe (2 cycles per warp instruction)
+      static_assert(kMaxS / 32 / kWarps <= 32, "one group per lane in the candidate pass");
+      const int g0 = w0 >> 5, ng = (w1 - w0 + 31) >> 5;  // (g0 is a multiple of 4: per is)
+      const uint32_t *kw = keys + (size_t)g0 * 32 + lane;
+      uint4 *gtp = reinterpret_cast<uint4 *>(sh.gtm + g0), *eqp = reinterpret_cast<uint4 *>(sh.eqm + g0);
+      const bool l0 = lane == 0;
+      int gi = 0;
+#pragma unroll 4
+      for (; gi + 4 <= ng; gi += 4) {
+        uint32_t kk[4], mg[4], me[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) kk[u] = kw[(gi + u) * 32];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          mg[u] = __ballot_sync(0xffffffffu, kk[u] >= gthr);
+          me[u] = __ballot_sync(0xffffffffu, kk[u] >= elo);
+        }
+        if (l0) {
+          gtp[gi >> 2] = make_uint4(mg[0], mg[1], mg[2], mg[3]);
+          eqp[gi >> 2] = make_uint4(me[0], me[1], me[2], me[3]);
+        }
       }
-      if (lane < ng) {
-        sh.gtm[g0 + lane] = ga;
-        sh.eqm[g0 + lane] = ea;
+      for (; gi < ng; ++gi) {
+        const uint32_t key = kw[gi * 32];
+        const uint32_t mg = __ballot_sync(0xffffffffu, key >= gthr);
+        const uint32_t me = __ballot_sync(0xffffffffu, key >= elo);
+        if (lane == 0) {
+          sh.gtm[g0 + gi] = mg;
+          sh.eqm[g0 + gi] = me;
+        }
       }
       __syncwarp();
       DS_TRACE_AT(1, 8);
       if (!whole1) {  // the D1 tokens: candidate list + digit-2 histogram (lane per group)
         const int ng = (w1 - w0 + 31) >> 5, grp = (w0 >> 5) + lane;
-        uint32_t e = lane < ng ? sh.eqm[grp] : 0u;
+        uint32_t e = lane < ng ? sh.eqm[grp] ^ sh.gtm[grp] : 0u;  // digit1 == D1
+        if (lane < ng) sh.eqm[grp] = e;
         const uint32_t ne = __popc(e);
         uint32_t incl = ne;
 #pragma unroll

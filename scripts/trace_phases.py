@@ -102,4 +102,11 @@ report(2, ["start", "rowids", "loop done", "cluster sync", "merged"])
 report(1, ["start", "streamed", "masks", "tail done", "gt rows done", "all rows", "merged"])
 report_slots(1, [(0, 12, "prologue"), (12, 13, "stream t0"), (13, 1, "stream sync"), (1, 7, "D1 boundary"), (7, 8, "mask loop w0"), (8, 9, "cand gather w0"), (9, 2, "sync"),
                  (2, 3, "tail"), (2, 14, "tail: level 2"), (14, 15, "tail: members"), (15, 3, "tail: rank+list"), (5, 10, "partials"), (10, 11, "weights"), (11, 6, "outputs")])
-report_slots(2, [(0, 1, "sample sync")])  # fused decode, high-mask threshold (kind 2's slots borrowed)
+report_slots(2, [(0, 1, "sample sync")])
+t1, t2 = buf[1].astype(np.int64), buf[2].astype(np.int64)
+ok = (t1[:, 0] > 0) & (t2[:, 2] > 0) & (t2[:, 4] > 0)
+if ok.any():  # fused decode prologue: start -> pdl waited -> n known -> tile waited -> stream starts (slot 12)
+    for a, b_, nm in [((1, 0), (2, 2), "pro: pdl wait"), ((2, 2), (2, 3), "pro: n known"), ((2, 3), (2, 4), "pro: tile+sync"),
+                      ((2, 4), (1, 12), "pro: qlab")]:
+        d = (np.where(True, [t1, t2][b_[0] - 1][ok, b_[1]], 0) - [t1, t2][a[0] - 1][ok, a[1]]) / 1e3
+        print(f"  sub {nm:14s} p50 {np.median(d):7.2f} p90 {np.percentile(d, 90):7.2f}")  # fused decode, high-mask threshold (kind 2's slots borrowed)
