@@ -515,6 +515,24 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         for (int u = 0; u < U; ++u) pv[u] = __ldg(reinterpret_cast<const uint4 *>(lab) + (size_t)(i0 + u * kThreads));
         rows8(i0, pv);
       }
+      if (i0 < nloc) {  // the last, partial batch: all its rows in flight at once (S = 4K: the only batch)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          pv[u] = i0 + u * kThreads < nloc ? __ldg(reinterpret_cast<const uint4 *>(lab) + (size_t)(i0 + u * kThreads))
+                                           : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (i0 + u * kThreads >= nloc) break;
+          const T *e = reinterpret_cast<const T *>(&pv[u]);
+          float s = 0.0f;
+#pragma unroll
+          for (int j = 0; j < R; ++j) s = fmaf(ql[j], Elem<T>::to_f(e[j]), s);
+          const uint32_t k0 = order_key(s);
+          keys[i0 + u * kThreads] = k0;
+          DS_HIST_ADD(&sh.h1[k0 >> kSh1]);
+        }
+        i0 = nloc;
+      }
     }
     for (int i = i0; i < nloc; i += kThreads) {
       const T *row = lab + (size_t)i * r;
@@ -1582,7 +1600,11 @@ cudaError_t launch_fused(const ds_cache *c, FusedParams p, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long units = (long)c->batch * (c->group_reduce == DS_GROUP_PER_HEAD ? c->num_q_heads : c->num_kv_heads);
+#ifdef DS_EXP_L2PF  // timing experiment: force the phase-0 L2 prefetch on (1) or off (0)
+    p.l2_prefetch = DS_EXP_L2PF;
+#else
     p.l2_prefetch = nch > 1 || units * nch > sms;
+#endif
   }
 #define DS_F(T)                                                                                         \
   if (c->head_dim == 64) return c->r == 8 ? launch_t<T, 8, 64>(c, p, nch, st) : launch_t<T, 0, 64>(c, p, nch, st); \

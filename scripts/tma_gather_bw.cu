@@ -248,6 +248,13 @@ int main(int argc, char **argv) {
            names[mode], ctas, warps, stages, smem / 1024, best * 1e3, bytes / best / 1e6, bytes / (sum / reps) / 1e6,
            nb, cudaGetErrorString(cudaGetLastError()));
   };
+  if (getenv("GATHER_CTAS")) {  // e.g. GATHER_CTAS=128: the c3 kernel's grid (units on 128 of the SMs)
+    const int c = atoi(getenv("GATHER_CTAS"));
+    run(0, c, 16, 2);
+    run(0, c, 16, 3);
+    run(0, sms, 16, 2);
+    return 0;
+  }
   for (int mode = 0; mode < 3; ++mode) {
     run(mode, sms, 16, 2);
     run(mode, sms, 16, 3);
