@@ -74,6 +74,7 @@ constexpr int kD3 = 1024;             // digit 3: key bits 9..0
 constexpr int kCandCap = 2048;        // digit-1 boundary tokens listed
 constexpr int kMaxMembers = 512;      // 22-bit-prefix boundary tokens ranked directly
 constexpr int kListCap = 2048 + 64;   // pool rows per attention round (k = 2048 + batch alignment)
+constexpr int kExtCap = 2 * kCandCap - 64;  // list positions continued in a dead candidate buffer
 constexpr int kBatch = 8;             // rows per warp batch
 constexpr int kBarAtt = 1, kBarSel = 2, kBarDone = 3, kBarRegs = 4;  // named barriers
 // register split after the common phases (64 per thread at launch):
@@ -751,6 +752,14 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     const int sl = t - pg * c.P;
     return ((uint32_t)__ldg(bt + pg) * (uint32_t)c.Hkv + (uint32_t)h) * (uint32_t)c.P + (uint32_t)sl;
   };
+  // list positions >= kListCap: the candidate buffer of the cluster-local
+  // tail (h1) or this CTA's own candidate list (past the 32 words the list
+  // building uses as scratch) -- both dead once every mark is in selm, and
+  // neither read by another CTA by then
+  static_assert(sizeof(Sh::h1) / 4 >= kExtCap && sizeof(Sh::cand) / 4 - 64 >= kExtCap, "extended list");
+  auto ext_list = [&](bool loc) -> uint32_t * {
+    return loc ? reinterpret_cast<uint32_t *>(sh.h1) : reinterpret_cast<uint32_t *>(sh.cand) + 64;
+  };
   if (tid == 0) {
     sh.state[14] = 0u;  // candidate rows not listed yet (read by the attention warps)
     sh.state[15] = 0u;  // the attention warps' batch cursor
@@ -1022,11 +1031,24 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         n_gt += sh.cand[w].x;
       }
       const uint32_t p0 = (n_gt + kBatch - 1) & ~(uint32_t)(kBatch - 1);  // batch-aligned start
-      const bool fits = p0 + n_sel <= (uint32_t)kListCap;
+      // positions past the list continue in a dead candidate buffer (split-S
+      // units select ~k / nch rows per CTA, which can exceed the list)
+      uint32_t *const xl = ext_list(loc);
+      // (n_gt > kListCap: the attention warps run the certain rows in rounds
+      // of the list, and the candidates after them, from selm)
+      const bool fits = n_gt <= (uint32_t)kListCap && p0 + n_sel <= (uint32_t)(kListCap + kExtCap);
       if (fits) {
         uint32_t pa = p0 + base + ia - ca, pb = p0 + base + ta + ib - cb;
-        for (uint32_t m = ma; m; m &= m - 1) sh.list[pa++] = row_of(t0 + ga * 32 + __ffs(m) - 1);
-        for (uint32_t m = mb; m; m &= m - 1) sh.list[pb++] = row_of(t0 + gb * 32 + __ffs(m) - 1);
+        for (uint32_t m = ma; m; m &= m - 1, ++pa) {
+          const uint32_t rw = row_of(t0 + ga * 32 + __ffs(m) - 1);
+          if (pa < (uint32_t)kListCap) sh.list[pa] = rw;
+          else xl[pa - kListCap] = rw;
+        }
+        for (uint32_t m = mb; m; m &= m - 1, ++pb) {
+          const uint32_t rw = row_of(t0 + gb * 32 + __ffs(m) - 1);
+          if (pb < (uint32_t)kListCap) sh.list[pb] = rw;
+          else xl[pb - kListCap] = rw;
+        }
       }
       sel_sync();
       if (stid == 0) {
@@ -1261,6 +1283,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         for (uint32_t m = ma; m; m &= m - 1) sh.list[pa++] = row_of(t0 + ga * 32 + __ffs(m) - 1);
         for (uint32_t m = mb; m; m &= m - 1) sh.list[pb++] = row_of(t0 + gb * 32 + __ffs(m) - 1);
         named_sync(kBarAtt, kAttThreads);  // the list of certain rows is complete
+        const uint32_t *const xl = ext_list(CL && tail && sh.state[2] <= (uint32_t)kCandCap);  // (loc)
         // batches of 8 list positions handed out by a shared cursor: batches
         // below nb1 are certain rows; the selected candidates follow from
         // position 8 * nb1 once the selection warps raise the flag
@@ -1291,7 +1314,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
             const int q = lane + 32 * m;
             const int rr = q / CHN, ch = q % CHN;
             const bool rv = rr < nv;
-            const size_t off = rv ? (size_t)sh.list[rb + rr] * ROWB + (size_t)ch * 16 : 0;
+            const int pos = rb + rr;
+            const uint32_t rid = !rv ? 0u : pos < kListCap ? sh.list[pos] : xl[pos - kListCap];
+            const size_t off = (size_t)rid * ROWB + (size_t)ch * 16;
             const uint32_t dst = smem_u32(st + rr * ROWB + swz(rr, ch));
             cp_async16(dst, kp + off, rv ? 16 : 0);
             cp_async16(dst + kBatch * ROWB, vp + off, rv ? 16 : 0);

@@ -238,3 +238,22 @@ def test_long_sequence_large_cluster(S, k):
     assert ds.ds_decode_launches(cache, k) == 1, "expected the single-kernel cluster path"
     y, idx = run_decode(cache, lay, k)
     check_units(lay, cache, C, k, all_units(cfg), y, idx)
+
+
+EXT = [
+    # name, cfg, seq_lens, k: more selected rows per CTA than the 2112-entry list,
+    # continued in the dead candidate buffer (one CTA, and 8-CTA clusters)
+    ("cta_k2150", synth.Config("x1", B=2, Hq=8, Hkv=1, d=128, S=8000, r=8, k=2150, dtype="bf16"), [8000, 7001], 2150),
+    ("cta_k3000", synth.Config("x2", B=2, Hq=8, Hkv=1, d=128, S=8000, r=8, k=3000, dtype="bf16"), [8000, 6500], 3000),
+    ("cluster8_k17600", synth.Config("x3", B=1, Hq=4, Hkv=1, d=128, S=65536, r=8, k=17600, dtype="bf16"), None, 17600),
+    ("cluster8_ragged", synth.Config("x4", B=2, Hq=4, Hkv=1, d=128, S=40000, r=8, k=18000, dtype="fp16"),
+     [40000, 33333], 18000),
+]
+
+
+@pytest.mark.parametrize("name,cfg,seq_lens,k", EXT, ids=[e[0] for e in EXT])
+def test_extended_row_list(name, cfg, seq_lens, k):
+    lay, cache, C = build_cache(cfg, seq_lens=seq_lens)
+    assert ds.ds_decode_launches(cache, k) == 1
+    y, idx = run_decode(cache, lay, k)
+    check_units(lay, cache, C, k, all_units(cfg), y, idx)
