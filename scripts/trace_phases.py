@@ -19,7 +19,7 @@ for kv in sys.argv[2:]:  # overrides, e.g. B=1 Hkv=1 Hq=4
     key, val = kv.split("=")
     cfg = cfg.with_(**{key: int(val)})
 print(cfg)
-lay = synth.make_layer(cfg, cfg.seed_base, device="cuda")
+lay = synth.make_layer(cfg, cfg.seed_base, device="cuda", structure=os.environ.get("DS_STRUCTURE", "iid"))
 cache = ds.LayerCache.allocate(cfg.B, cfg.Hq, cfg.Hkv, cfg.d, cfg.S, cfg.r, synth.DTYPES[cfg.dtype], lay.block_table,
                                num_pages=lay.num_pages, page_size=cfg.page_size, channel_idx=lay.C_plant,
                                label_format=os.environ.get("DS_LABEL", "native"))
