@@ -194,11 +194,13 @@ __device__ __forceinline__ uint32_t cluster_sum(int nch, F &&load) {
   return s;
 }
 
-// CL: a cluster of CTAs per unit.  PLAIN: the 16-bit label and the group-sum
-// reading fixed at compile time (the serving variant: the label-format / GQA
-// branches are compiled out, so its code is compact -- the serial phases
-// between the streams are otherwise slowed by instruction-cache misses)
-template <typename T, int R, int D, bool CL, bool PLAIN>
+// CL: a cluster of CTAs per unit.  PV: the label format and the group-sum
+// reading fixed at compile time -- 1: the 16-bit label (the serving
+// variant), 2: the 4-bit label (R16) -- so the label-format / GQA branches
+// are compiled out and the code is compact (the serial phases between the
+// streams are otherwise slowed by instruction-cache misses); 0: every
+// format and GQA reading chosen at run time
+template <typename T, int R, int D, bool CL, int PV>
 __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   using GE = Geo<D>;
   constexpr int ROWB = GE::ROWB, CHN = GE::CHN, STAGE = GE::STAGE;
@@ -215,8 +217,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     else return ptr;
   };
   const CacheView &c = p.c;
-  const bool lq4 = !PLAIN && c.lq4, lnone = !PLAIN && c.lnone;     // label format (R16 / Table 4)
-  const int greduce = PLAIN ? (int)DS_GROUP_SUM : (int)c.greduce;  // GQA reading (R3 / R17)
+  const bool lq4 = PV == 2 || (PV == 0 && c.lq4), lnone = PV == 0 && c.lnone;  // label format (R16 / Table 4)
+  const int greduce = PV ? (int)DS_GROUP_SUM : (int)c.greduce;                 // GQA reading (R3 / R17)
   // a unit is one (b, KV head) -- or one (b, query head) for DS_GROUP_PER_HEAD
   // (reading R17: each query head selects on its own over its KV head's data)
   const bool perh = greduce == DS_GROUP_PER_HEAD;
@@ -1487,15 +1489,15 @@ static size_t smem_bytes(int chunk) {
   return sizeof(Sh) + region;
 }
 
-template <typename T, int R, int D, bool CL, bool PLAIN>
+template <typename T, int R, int D, bool CL, int PV>
 static cudaError_t launch_cl(const ds_cache *c, const FusedParams &p, int nch, cudaStream_t st) {
   const size_t smem = smem_bytes<T, R, D>(p.chunk);
   static PerDeviceOnce once;
   const cudaError_t attr = once([] {
-    cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, R, D, CL, PLAIN>,
+    cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, R, D, CL, PV>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedMaxSmem);
     if (e == cudaSuccess && CL)
-      e = cudaFuncSetAttribute(decode_kernel<T, R, D, CL, PLAIN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      e = cudaFuncSetAttribute(decode_kernel<T, R, D, CL, PV>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return e;
   });
   if (attr != cudaSuccess) return attr;
@@ -1514,16 +1516,20 @@ static cudaError_t launch_cl(const ds_cache *c, const FusedParams &p, int nch, c
   a[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = CL ? a : a + 1;  // no cluster attribute for one CTA per unit
   cfg.numAttrs = CL ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, decode_kernel<T, R, D, CL, PLAIN>, p);
+  return cudaLaunchKernelEx(&cfg, decode_kernel<T, R, D, CL, PV>, p);
 }
 
 template <typename T, int R, int D>
 static cudaError_t launch_t(const ds_cache *c, const FusedParams &p, int nch, cudaStream_t st) {
-  // the serving variant (16-bit label, group sum) has its own compact instance
-  const bool plain = R > 0 && c->label_format == DS_LABEL_NATIVE && c->group_reduce == DS_GROUP_SUM;
-  if (nch > 1)
-    return plain ? launch_cl<T, R, D, true, true>(c, p, nch, st) : launch_cl<T, R, D, true, false>(c, p, nch, st);
-  return plain ? launch_cl<T, R, D, false, true>(c, p, nch, st) : launch_cl<T, R, D, false, false>(c, p, nch, st);
+  // the group-sum reading with the 16-bit or the 4-bit label (r = 8) has its
+  // own compact instance
+  if constexpr (R > 0) {
+    if (c->group_reduce == DS_GROUP_SUM && c->label_format == DS_LABEL_NATIVE)
+      return nch > 1 ? launch_cl<T, R, D, true, 1>(c, p, nch, st) : launch_cl<T, R, D, false, 1>(c, p, nch, st);
+    if (c->group_reduce == DS_GROUP_SUM && c->label_format == DS_LABEL_INT4)
+      return nch > 1 ? launch_cl<T, R, D, true, 2>(c, p, nch, st) : launch_cl<T, R, D, false, 2>(c, p, nch, st);
+  }
+  return nch > 1 ? launch_cl<T, R, D, true, 0>(c, p, nch, st) : launch_cl<T, R, D, false, 0>(c, p, nch, st);
 }
 
 // Can a cluster of nch CTAs (1024 threads, ~200 KB of shared memory each) be
@@ -1534,10 +1540,10 @@ static bool cluster_fits_t(int nch, int chunk) {
   if (nch <= 8) return true;
   static PerDeviceOnce once;
   if (once([] {
-        cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, R, D, true, false>,
+        cudaError_t e = cudaFuncSetAttribute(decode_kernel<T, R, D, true, 0>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedMaxSmem);
         if (e == cudaSuccess)
-          e = cudaFuncSetAttribute(decode_kernel<T, R, D, true, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+          e = cudaFuncSetAttribute(decode_kernel<T, R, D, true, 0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         return e;
       }) != cudaSuccess)
     return false;
@@ -1553,7 +1559,7 @@ static bool cluster_fits_t(int nch, int chunk) {
   cfg.attrs = a;
   cfg.numAttrs = 1;
   int nclusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&nclusters, decode_kernel<T, R, D, true, false>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&nclusters, decode_kernel<T, R, D, true, 0>, &cfg) != cudaSuccess) {
     cudaGetLastError();  // clear the sticky-free error of the query
     return false;
   }
