@@ -467,15 +467,20 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       const uint4 *cv = reinterpret_cast<const uint4 *>(cod);
       const uint2 *sv = reinterpret_cast<const uint2 *>(scl);
       const int ng = nloc >> 2;
-      auto grp = [&](int g, const uint4 &v, const uint2 &w) {
-        const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-        const T *se = reinterpret_cast<const T *>(&w);
-        uint32_t kk[4];
+      u64 qp[8];  // {q_label[j], q_label[j]} for the packed-pair chains (R == 8 here)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          kk[e] = order_key(q4_word_dot(wd[e], ql, 0.0f) * Elem<T>::to_f(se[e]));
-          DS_HIST_ADD(&sh.h1[kk[e] >> kSh1]);
-        }
+      for (int j = 0; j < 8; ++j) qp[j] = pack_u2(__float_as_uint(ql[R == 8 ? j : 0]), __float_as_uint(ql[R == 8 ? j : 0]));
+      auto grp = [&](int g, const uint4 &v, const uint2 &w) {
+        // tokens (0, 1) and (2, 3) of the group as fp32 pairs: s_hat = chain * s
+        const T *se = reinterpret_cast<const T *>(&w);
+        const float2 d01 = q4_pair_dot(v.x, v.y, qp), d23 = q4_pair_dot(v.z, v.w, qp);
+        const float2 p01 = unpack_f2(fmul2(pack_u2(__float_as_uint(d01.x), __float_as_uint(d01.y)),
+                                           pack_u2(__float_as_uint(Elem<T>::to_f(se[0])), __float_as_uint(Elem<T>::to_f(se[1])))));
+        const float2 p23 = unpack_f2(fmul2(pack_u2(__float_as_uint(d23.x), __float_as_uint(d23.y)),
+                                           pack_u2(__float_as_uint(Elem<T>::to_f(se[2])), __float_as_uint(Elem<T>::to_f(se[3])))));
+        const uint32_t kk[4] = {order_key(p01.x), order_key(p01.y), order_key(p23.x), order_key(p23.y)};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) DS_HIST_ADD(&sh.h1[kk[e] >> kSh1]);
         *reinterpret_cast<uint4 *>(keys + 4 * g) = make_uint4(kk[0], kk[1], kk[2], kk[3]);
       };
       // two groups per thread in flight while the previous two are scored

@@ -190,6 +190,54 @@ __device__ __forceinline__ float q4_word_dot(uint32_t w, const float *ql, float 
   acc = fmaf(ql[7], c7, acc);
   return acc;
 }
+// Two 4-bit label rows at once with packed fp32 pairs (sm_100 FADD2 /
+// FFMA2): each lane of add.rn.f32x2 / fma.rn.f32x2 is the scalar RN
+// operation, so both chains are bit-identical to q4_word_dot's (same codes,
+// same j order).  A pair instruction issues in 2 cycles against 1 for the
+// scalar one -- the same fp32 rate -- but half the issue slots, and the
+// 4-bit stream is issue-bound (~40 instructions per token with scalars).
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pack_u2(uint32_t lo, uint32_t hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 unpack_f2(u64 v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ u64 fadd2(u64 x, u64 y) {
+  u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+  return r;
+}
+__device__ __forceinline__ u64 fmul2(u64 x, u64 y) {
+  u64 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+  return r;
+}
+__device__ __forceinline__ void ffma2(u64 &acc, u64 x, u64 y) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(x), "l"(y));
+}
+template <uint32_t MASK, uint32_t E, uint32_t NEGK>
+__device__ __forceinline__ u64 q4_code2(uint32_t a, uint32_t b) {  // {c_j of a, c_j of b} as exact fp32
+  return fadd2(pack_u2(lop3_and_or<MASK>(a, E), lop3_and_or<MASK>(b, E)), ((u64)NEGK << 32) | NEGK);
+}
+// qp[j] = {q_label[j], q_label[j]}; returns the two chains (no scale)
+__device__ __forceinline__ float2 q4_pair_dot(uint32_t wa, uint32_t wb, const u64 *qp) {
+  const uint32_t a = wa ^ 0x88888888u, as = a >> 20, b = wb ^ 0x88888888u, bs = b >> 20;
+  u64 acc = 0ull;  // {+0, +0}, as q4_word_dot's acc = 0
+  ffma2(acc, qp[0], q4_code2<0x0000Fu, 0x4B000000u, 0xcb000008u>(a, b));  // - (2^23 + 8)
+  ffma2(acc, qp[1], q4_code2<0x000F0u, 0x49000000u, 0xc9000080u>(a, b));  // - (2^19 + 8)
+  ffma2(acc, qp[2], q4_code2<0x00F00u, 0x47000000u, 0xc7000800u>(a, b));  // - (2^15 + 8)
+  ffma2(acc, qp[3], q4_code2<0x0F000u, 0x45000000u, 0xc5008000u>(a, b));  // - (2^11 + 8)
+  ffma2(acc, qp[4], q4_code2<0xF0000u, 0x43000000u, 0xc3080000u>(a, b));  // - (2^7 + 8)
+  ffma2(acc, qp[5], q4_code2<0x0000Fu, 0x4B000000u, 0xcb000008u>(as, bs));
+  ffma2(acc, qp[6], q4_code2<0x000F0u, 0x49000000u, 0xc9000080u>(as, bs));
+  ffma2(acc, qp[7], q4_code2<0x00F00u, 0x47000000u, 0xc7000800u>(as, bs));
+  return unpack_f2(acc);
+}
 // 16-B / 8-B read-only loads issued where they are written (asm volatile:
 // the compiler cannot sink a prefetch below the work it overlaps)
 __device__ __forceinline__ uint4 ldg_nc_v4(const void *p) {

@@ -6,7 +6,10 @@
 typedef unsigned long long u64;
 __device__ __forceinline__ u64 f2(float a, float b) { return (u64)__float_as_uint(a) | ((u64)__float_as_uint(b) << 32); }
 template <int MODE>
-__global__ void k(float *out, long long *cyc, int n, float m) {
+__global__ void k(float *out, long long *cyc, int n, float m0) {
+  // per-thread multiplier (a plain register, not a uniform / constant operand:
+  // FFMA with a uniform or immediate operand issues at twice the 3-register rate)
+  const float m = m0 + threadIdx.x * 1e-9f;
   float a[16];
   u64 p[8];
 #pragma unroll
