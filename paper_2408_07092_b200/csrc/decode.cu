@@ -235,11 +235,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&sh.xbar[i])), "r"(nch) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  {
-    // The label rows of this CTA's chunk (and its block-table slice) go to L2
-    // before the wait: the preceding kernel does not produce them (it may
-    // write one new row, which the L2 keeps coherent; they are read into
-    // registers only after the wait), so their HBM reads overlap its drain.
+  // The label rows of this CTA's chunk (and its block-table slice) go to L2
+  // before the wait: the preceding kernel does not produce them (it may
+  // write one new row, which the L2 keeps coherent; they are read into
+  // registers only after the wait), so their HBM reads overlap its drain.
+  auto l2_prefetch_chunk = [&] {
     const int t0p = crank * p.chunk, mloc = max(0, min(p.chunk, c.Smax - t0p));
     const size_t lr0 = ((size_t)b * c.Hkv + h) * (size_t)c.Smax + t0p;
     if (!p.l2_prefetch) {
@@ -255,7 +255,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       const int32_t *btp = c.block_table + (size_t)b * c.maxp + pg0;
       if (((uintptr_t)btp & 15) == 0) prefetch_l2(btp, (size_t)min(npg, c.maxp - pg0) * 4 & ~(size_t)15);
     }
-  }
+  };
+  l2_prefetch_chunk();
   pdl_wait();  // label / KV rows may come from the preceding append
   // (dependents are released only after the register split below: a CTA of
   // the next kernel must not take the registers the selection warps free)
