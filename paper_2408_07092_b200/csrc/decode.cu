@@ -1572,6 +1572,45 @@ static bool cluster_fits_t(int nch, int chunk) {
   return nclusters > 0;
 }
 
+// How many clusters of n CTAs can be co-resident (1 CTA per SM at the fused
+// kernel's footprint; a cluster lives in one GPC, so this is GPC-limited, not
+// SMs / n).  Queried once per device for n = 2, 4, 8, 16 -- every instance of
+// decode_kernel has the same footprint (1024 threads, ~200 KB of shared
+// memory, whole SM).  0 when the query fails.
+static int max_active_clusters(int n) {
+  static PerDeviceOnce once;
+  static int mac[kMaxDevices][4];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
+  const cudaError_t e = once([dev] {
+    auto kern = decode_kernel<__nv_bfloat16, 8, 128, true, 0>;
+    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedMaxSmem);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int i = 0; i < 4 && r == cudaSuccess; ++i) {
+      const int m = 2 << i;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(m, 1);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = smem_bytes<__nv_bfloat16, 8, 128>(kMaxS);
+      cudaLaunchAttribute a[1];
+      a[0].id = cudaLaunchAttributeClusterDimension;
+      a[0].val.clusterDim.x = m;
+      a[0].val.clusterDim.y = 1;
+      a[0].val.clusterDim.z = 1;
+      cfg.attrs = a;
+      cfg.numAttrs = 1;
+      int nc = 0;
+      r = cudaOccupancyMaxActiveClusters(&nc, kern, &cfg);
+      mac[dev][i] = nc;
+    }
+    if (r != cudaSuccess) cudaGetLastError();  // (not sticky)
+    return r;
+  });
+  if (e != cudaSuccess) return 0;
+  const int i = n == 2 ? 0 : n == 4 ? 1 : n == 8 ? 2 : n == 16 ? 3 : -1;
+  return i < 0 ? 0 : mac[dev][i];
+}
+
 }  // namespace fused
 
 // CTAs per unit (one thread-block cluster): enough to cover the SMs when
@@ -1581,12 +1620,24 @@ int fused_cluster(const ds_cache *c) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int units = c->batch * (c->group_reduce == DS_GROUP_PER_HEAD ? c->num_q_heads : c->num_kv_heads);
-  int nch = units * 4 >= sms * 3 ? 1 : sms / units;
-  if (nch > 8) nch = 8;
-  // short sequences: a cluster's fixed exchange cost (~4-5 us) outweighs the
-  // split streaming/gather time (measured on c2, B=1 MHA: S=4K one CTA per
-  // unit 15.9 us vs 18.1 us for a cluster of 4; S=16K even; S=32K 4 CTAs win)
-  if (c->max_seq_len <= 8192) nch = 1;
+  // A cluster of CTAs per unit when the units cover < 3/4 of the SMs and the
+  // sequences are long enough: the largest power of two n <= 16 whose
+  // clusters of every unit are co-resident in one wave (units * n <= SMs and
+  // units <= the clusters of n the GPCs can hold -- 16 clusters of 8 do not
+  // all fit on B200 and took a second wave: 16 units of S=32K, 34.7 us with 8
+  // CTAs vs 20.4 us with 4) with chunks of >= 4K tokens.  Short sequences
+  // (<= 8K) stay on one CTA: a cluster's fixed exchange cost outweighs the
+  // split streaming/gather time (c2 S=4K: 12.6 us on one CTA, 14.0 on 4;
+  // S=16K: 4 CTAs 17.3 us vs 18.9 on 2 and 22.1 on 1).
+  int nch = 1;
+  if (units * 4 < sms * 3 && c->max_seq_len > 8192) {
+    for (int n = 16; n >= 2; n >>= 1) {
+      if (n * units > sms || (c->max_seq_len + n - 1) / n < 4096) continue;
+      if (fused::max_active_clusters(n) < units) continue;
+      nch = n;
+      break;
+    }
+  }
   const int need = (c->max_seq_len + fused::kMaxS - 1) / fused::kMaxS;
 #ifdef DS_EXP_NCH_ENV  // timing experiments only (never in libds.so): DS_NCH forces the cluster size
   if (const char *e = getenv("DS_NCH")) {
