@@ -1574,20 +1574,19 @@ static bool cluster_fits_t(int nch, int chunk) {
 
 // How many clusters of n CTAs can be co-resident (1 CTA per SM at the fused
 // kernel's footprint; a cluster lives in one GPC, so this is GPC-limited, not
-// SMs / n).  Queried once per device for n = 2, 4, 8, 16 -- every instance of
+// SMs / n).  Queried once per device for n = 2..16 -- every instance of
 // decode_kernel has the same footprint (1024 threads, ~200 KB of shared
 // memory, whole SM).  0 when the query fails.
 static int max_active_clusters(int n) {
   static PerDeviceOnce once;
-  static int mac[kMaxDevices][4];
+  static int mac[kMaxDevices][17];
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
+  if (n < 2 || n > 16 || cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
   const cudaError_t e = once([dev] {
     auto kern = decode_kernel<__nv_bfloat16, 8, 128, true, 0>;
     cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedMaxSmem);
     if (r == cudaSuccess) r = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    for (int i = 0; i < 4 && r == cudaSuccess; ++i) {
-      const int m = 2 << i;
+    for (int m = 2; m <= 16 && r == cudaSuccess; ++m) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(m, 1);
       cfg.blockDim = dim3(kThreads);
@@ -1601,14 +1600,12 @@ static int max_active_clusters(int n) {
       cfg.numAttrs = 1;
       int nc = 0;
       r = cudaOccupancyMaxActiveClusters(&nc, kern, &cfg);
-      mac[dev][i] = nc;
+      mac[dev][m] = nc;
     }
     if (r != cudaSuccess) cudaGetLastError();  // (not sticky)
     return r;
   });
-  if (e != cudaSuccess) return 0;
-  const int i = n == 2 ? 0 : n == 4 ? 1 : n == 8 ? 2 : n == 16 ? 3 : -1;
-  return i < 0 ? 0 : mac[dev][i];
+  return e == cudaSuccess ? mac[dev][n] : 0;
 }
 
 }  // namespace fused
@@ -1621,18 +1618,19 @@ int fused_cluster(const ds_cache *c) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int units = c->batch * (c->group_reduce == DS_GROUP_PER_HEAD ? c->num_q_heads : c->num_kv_heads);
   // A cluster of CTAs per unit when the units cover < 3/4 of the SMs and the
-  // sequences are long enough: the largest power of two n <= 16 whose
-  // clusters of every unit are co-resident in one wave (units * n <= SMs and
-  // units <= the clusters of n the GPCs can hold -- 16 clusters of 8 do not
-  // all fit on B200 and took a second wave: 16 units of S=32K, 34.7 us with 8
-  // CTAs vs 20.4 us with 4) with chunks of >= 4K tokens.  Short sequences
-  // (<= 8K) stay on one CTA: a cluster's fixed exchange cost outweighs the
-  // split streaming/gather time (c2 S=4K: 12.6 us on one CTA, 14.0 on 4;
-  // S=16K: 4 CTAs 17.3 us vs 18.9 on 2 and 22.1 on 1).
+  // sequences are long enough: the largest n <= 16 whose clusters of every
+  // unit are co-resident in one wave (units * n <= SMs and units <= the
+  // clusters of n the GPCs can hold) with chunks of >= 4K tokens.  Past the
+  // co-residency limit a second wave doubles the time (16 units of S=32K:
+  // 4/5/6 CTAs 20.4/19.9/19.3 us, 7 and 8 CTAs 35.5/34.7 us; 16 units of
+  // S=128K: 4/6 CTAs 43.1/34.7 us, 7 CTAs 60.3 us).  Short sequences (<= 8K)
+  // stay on one CTA: a cluster's fixed exchange cost outweighs the split
+  // streaming/gather time (c2 S=4K: 12.6 us on one CTA, 14.0 on 4; S=16K:
+  // 4 CTAs 17.3 us vs 18.9 on 2 and 22.1 on 1).
   int nch = 1;
   if (units * 4 < sms * 3 && c->max_seq_len > 8192) {
-    for (int n = 16; n >= 2; n >>= 1) {
-      if (n * units > sms || (c->max_seq_len + n - 1) / n < 4096) continue;
+    for (int n = min(16, sms / units); n >= 2; --n) {
+      if ((c->max_seq_len + n - 1) / n < 4096) continue;
       if (fused::max_active_clusters(n) < units) continue;
       nch = n;
       break;

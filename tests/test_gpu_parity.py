@@ -245,9 +245,11 @@ EXT = [
     # continued in the dead candidate buffer (one CTA, and 8-CTA clusters)
     ("cta_k2150", synth.Config("x1", B=2, Hq=8, Hkv=1, d=128, S=8000, r=8, k=2150, dtype="bf16"), [8000, 7001], 2150),
     ("cta_k3000", synth.Config("x2", B=2, Hq=8, Hkv=1, d=128, S=8000, r=8, k=3000, dtype="bf16"), [8000, 6500], 3000),
-    ("cluster8_k17600", synth.Config("x3", B=1, Hq=4, Hkv=1, d=128, S=65536, r=8, k=17600, dtype="bf16"), None, 17600),
-    ("cluster8_ragged", synth.Config("x4", B=2, Hq=4, Hkv=1, d=128, S=40000, r=8, k=18000, dtype="fp16"),
-     [40000, 33333], 18000),
+    # (one unit of S=64K: 16 CTAs of 4K tokens; two of S=40000: 9 CTAs of 4.4K)
+    ("cluster16_k36000", synth.Config("x3", B=1, Hq=4, Hkv=1, d=128, S=65536, r=8, k=36000, dtype="bf16"), None,
+     36000),
+    ("cluster9_ragged", synth.Config("x4", B=2, Hq=4, Hkv=1, d=128, S=40000, r=8, k=21000, dtype="fp16"),
+     [40000, 33333], 21000),
 ]
 
 
