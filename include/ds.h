@@ -201,10 +201,11 @@ ds_status ds_decode_attention(const ds_cache *c, const void *q, int32_t k, void 
  * enqueues (0 on invalid arguments): 1 when the whole of Algorithm 1 runs
  * as one kernel (16-bit KV: one CTA per (b, KV head) unit, or a thread-block
  * cluster of up to 16 CTAs per unit when units are few or max_seq_len >
- * 32768 -- up to 512K tokens, clusters above 8 CTAs only where the occupancy
- * API says one can be resident), else 2 (fp32, or a cluster that cannot be
- * resident: score+select with the CTAs of a unit in one thread-block
- * cluster, then the attention).  Results are identical up to the fp32
+ * 32768 -- up to 512K tokens; when units are few, the largest cluster size
+ * whose clusters of all units the occupancy API says are co-resident in one
+ * wave; above 8 CTAs only where one can be resident), else 2 (fp32, or a
+ * cluster that cannot be resident: score+select with the CTAs of a unit in
+ * one thread-block cluster, then the attention).  Results are identical up to the fp32
  * summation order of the attention.  DS_GROUP_PER_HEAD exists only on the
  * one-kernel path (DS_ERR_UNSUPPORTED from the decode calls otherwise). */
 int32_t ds_decode_launches(const ds_cache *c, int32_t k);
