@@ -250,7 +250,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         prefetch_l2((const uint8_t *)c.label + lr0 * c.rb, (size_t)mloc * c.rb);
         prefetch_l2((const T *)c.label_scale + lr0, (size_t)mloc * sizeof(T));
       }
-    } else if (tid == 32) {
+    }
+    // the block-table slice (the row ids of the gathers) always: a few KB,
+    // L2-resident by the time the selected rows are looked up (c3 40.9 ->
+    // 40.8 us)
+    if (tid == 32) {
       const int pg0 = t0p / c.P, npg = (mloc + c.P - 1) / c.P + 1;
       const int32_t *btp = c.block_table + (size_t)b * c.maxp + pg0;
       if (((uintptr_t)btp & 15) == 0) prefetch_l2(btp, (size_t)min(npg, c.maxp - pg0) * 4 & ~(size_t)15);
