@@ -878,6 +878,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       }
       sel_sync();
     }
+#ifdef DS_TRACE  // (trace build: the D1-bin candidate count this CTA's tail ranks)
+    if (stid == 0 && blockIdx.x + blockIdx.y * gridDim.x < (unsigned)ds::kTraceCtas)
+      ds::g_trace[2][blockIdx.x + blockIdx.y * gridDim.x][7] =
+          1000000ull + (loc ? sh.state[2] : (!ovf ? sh.ncand : 999999u)) + (tail ? 0ull : 2000000ull);
+#endif
     if (tail) {
       boundary1024(sh.h2, sh.c2, need1, sh.state + 3, 0);
       DS_TRACE_BY(1, 14, kAttThreads);

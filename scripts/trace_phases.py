@@ -110,3 +110,9 @@ if ok.any():  # fused decode prologue: start -> pdl waited -> n known -> tile wa
                       ((2, 4), (1, 12), "pro: qlab")]:
         d = (np.where(True, [t1, t2][b_[0] - 1][ok, b_[1]], 0) - [t1, t2][a[0] - 1][ok, a[1]]) / 1e3
         print(f"  sub {nm:14s} p50 {np.median(d):7.2f} p90 {np.percentile(d, 90):7.2f}")  # fused decode, high-mask threshold (kind 2's slots borrowed)
+
+_nc = buf[2][:, 7].astype(np.int64)
+_nc = _nc[(_nc > 0) & (_nc < 2000000)] - 1000000
+if len(_nc):
+    print("  D1-bin candidates ranked by the tail (per CTA, tail only): p50", np.median(_nc), "p90",
+          np.percentile(_nc, 90), "max", _nc.max(), "n", len(_nc))
