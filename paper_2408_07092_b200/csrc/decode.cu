@@ -634,6 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   const int ngrp = (nloc + 31) >> 5;
   uint32_t D1 = 0, need1 = 0;
   bool whole1 = true, ovf = false;
+  uint32_t nd1 = 0;  // this CTA's D1 tokens (an upper bound of its selected candidates)
   if (!all_sel) {
     if (!CL) {  // 64 coarse bins of 64: 4 bins per thread, 16 lanes per coarse bin
       const uint4 f = reinterpret_cast<const uint4 *>(sh.h1)[tid];
@@ -666,7 +667,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
     D1 = sh.state[0];
     need1 = (uint32_t)keff - sh.state[1];
     whole1 = sh.state[2] == need1;
-    ovf = !whole1 && sh.h1[D1] > (uint32_t)kCandCap;  // this CTA's D1 tokens do not fit the list
+    nd1 = whole1 ? 0u : sh.h1[D1];
+    ovf = nd1 > (uint32_t)kCandCap;  // this CTA's D1 tokens do not fit the list
   }
   DS_TRACE_AT(1, 7);
   const bool tail = !all_sel && !whole1;
@@ -769,6 +771,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
   // building uses as scratch) -- both dead once every mark is in selm, and
   // neither read by another CTA by then
   static_assert(sizeof(Sh::h1) / 4 >= kExtCap && sizeof(Sh::cand) / 4 - 64 >= kExtCap, "extended list");
+  // more certain rows than the list holds: the whole selection still fits
+  // the list + its extension (this CTA selects at most its nd1 D1 tokens
+  // beyond the certain rows), so no attention rounds
+  auto ext_fits = [&](uint32_t n_gt) {
+    return ((n_gt + kBatch - 1) & ~(uint32_t)(kBatch - 1)) + nd1 <= (uint32_t)(kListCap + kExtCap);
+  };
   auto ext_list = [&](bool loc) -> uint32_t * {
     return loc ? reinterpret_cast<uint32_t *>(sh.h1) : reinterpret_cast<uint32_t *>(sh.cand) + 64;
   };
@@ -1051,9 +1059,34 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
       // positions past the list continue in a dead candidate buffer (split-S
       // units select ~k / nch rows per CTA, which can exceed the list)
       uint32_t *const xl = ext_list(loc);
-      // (n_gt > kListCap: the attention warps run the certain rows in rounds
-      // of the list, and the candidates after them, from selm)
-      const bool fits = n_gt <= (uint32_t)kListCap && p0 + n_sel <= (uint32_t)(kListCap + kExtCap);
+      // (n_gt > kListCap without ext_fits: the attention warps run the
+      // certain rows in rounds of the list, and the candidates after them,
+      // from selm)
+      const bool fits = (n_gt <= (uint32_t)kListCap || ext_fits(n_gt)) && p0 + n_sel <= (uint32_t)(kListCap + kExtCap);
+      if (fits && n_gt > (uint32_t)kListCap) {
+        // the certain rows past the list, at the positions the attention
+        // warps' list order gives them (warp sw = attention warp sw's groups)
+        const uint32_t xa = ga < ngrp ? sh.gtm[ga] : 0u, xb = gb < ngrp ? sh.gtm[gb] : 0u;
+        const uint32_t za = __popc(xa), zb = __popc(xb);
+        uint32_t ja = za, jb = zb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t ya = __shfl_up_sync(0xffffffffu, ja, o);
+          const uint32_t yb = __shfl_up_sync(0xffffffffu, jb, o);
+          if (lane >= o) {
+            ja += ya;
+            jb += yb;
+          }
+        }
+        const uint32_t sa = __shfl_sync(0xffffffffu, ja, 31);
+        uint32_t gbase = 0;
+        for (int w = 0; w < sw; ++w) gbase += sh.cand[w].x;
+        uint32_t qa = gbase + ja - za, qb = gbase + sa + jb - zb;
+        for (uint32_t m = xa; m; m &= m - 1, ++qa)
+          if (qa >= (uint32_t)kListCap) xl[qa - kListCap] = row_of(t0 + ga * 32 + __ffs(m) - 1);
+        for (uint32_t m = xb; m; m &= m - 1, ++qb)
+          if (qb >= (uint32_t)kListCap) xl[qb - kListCap] = row_of(t0 + gb * 32 + __ffs(m) - 1);
+      }
       if (fits) {
         uint32_t pa = p0 + base + ia - ca, pb = p0 + base + ta + ib - cb;
         for (uint32_t m = ma; m; m &= m - 1, ++pa) {
@@ -1295,10 +1328,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
         if (w < aw) base += x;
         n_gt += x;
       }
-      if (n_gt <= (uint32_t)kListCap) {
+      if (n_gt <= (uint32_t)kListCap || ext_fits(n_gt)) {
+        // certain rows at list positions [0, n_gt): those past the list are
+        // written by the selection warps with the candidates (below)
         uint32_t pa = base + ia - ca, pb = base + ta + ib - cb;
-        for (uint32_t m = ma; m; m &= m - 1) sh.list[pa++] = row_of(t0 + ga * 32 + __ffs(m) - 1);
-        for (uint32_t m = mb; m; m &= m - 1) sh.list[pb++] = row_of(t0 + gb * 32 + __ffs(m) - 1);
+        for (uint32_t m = ma; m && pa < (uint32_t)kListCap; m &= m - 1) sh.list[pa++] = row_of(t0 + ga * 32 + __ffs(m) - 1);
+        for (uint32_t m = mb; m && pb < (uint32_t)kListCap; m &= m - 1) sh.list[pb++] = row_of(t0 + gb * 32 + __ffs(m) - 1);
         named_sync(kBarAtt, kAttThreads);  // the list of certain rows is complete
         const uint32_t *const xl = ext_list(CL && tail && sh.state[2] <= (uint32_t)kCandCap);  // (loc)
         // batches of 8 list positions handed out by a shared cursor: batches
@@ -1309,7 +1344,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_kernel(FusedParams p) {
           int j = 0, nv = 0;
           if (lane == 0) {
             j = (int)atomicAdd(&sh.state[15], 1u);
-            if (j < nb1) {
+            if (j < nb1 && (j + 1) * kBatch <= kListCap) {
+              nv = min(kBatch, (int)n_gt - j * kBatch);
+            } else if (j < nb1) {  // certain rows past the list: listed with the candidates
+              while (*reinterpret_cast<volatile uint32_t *>(&sh.state[14]) == 0u) __nanosleep(64);
+              __threadfence_block();
               nv = min(kBatch, (int)n_gt - j * kBatch);
             } else {
               uint32_t f;
